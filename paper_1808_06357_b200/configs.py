@@ -1,0 +1,100 @@
+"""The five BASELINE.json configurations as (lattice, problem, time grid).
+
+Seed schedule: base seed 0x180806357 + config index;
+one SplitMix64 stream draws a_1..a_d ~ U[0.5,1.5], b_1..b_{d-1} ~ U[0,0.5],
+then (single wave function) c_1..c_d ~ U[c_lo,c_hi], p_1..p_d ~ U{-p..p};
+ensemble member m draws (c, p) from a stream seeded with
+SplitMix64(base ^ (m+1)).next(). v and z are shared by all members.
+
+Generating vectors: paper_1808_06357_b200/catalog.json holds the prime-n CBC
+vectors (recomputed and compared by tests/test_cbc.py); the rank-2 lattice
+of config 2 is Z = [(1,3,...,15), (0,1,3,...,13)], n = (4096, 4096)
+(SURVEY.md §7 step 1), validated by Lattice.create like any other.
+"""
+from __future__ import annotations
+
+import json
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import Lattice, cbc_construct, problem_draw
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SEED_BASE = 0x180806357
+
+
+@dataclass
+class Config:
+    name: str
+    index: int
+    d: int
+    rank: int
+    N: int                     # points (rank-2: n1*n2)
+    moduli: tuple
+    eps: float
+    T: float
+    m: int
+    sigma: float
+    batch: int
+    c_range: tuple
+    p_max: int
+    gen: list = field(default_factory=list)  # rank columns of length d
+
+    @property
+    def dt(self) -> float:
+        return self.T / self.m
+
+    @property
+    def seed(self) -> int:
+        return SEED_BASE + self.index
+
+
+def _catalog():
+    with open(os.path.join(_HERE, "catalog.json")) as f:
+        return json.load(f)
+
+
+def _c(name, index, d, n, eps, T, m, sigma, batch=1, c_range=(0.4, 0.6), p_max=2, rank=1, moduli=None, gen=None):
+    return Config(name, index, d, rank, int(np.prod(moduli)) if moduli else n, tuple(moduli or (n,)), eps, T, m,
+                  sigma, batch, c_range, p_max, gen or [])
+
+
+CONFIGS = {
+    "C0": _c("C0", 0, 2, 4099, 0.1, 1.0, 256, 0.1),
+    "C1": _c("C1", 1, 6, 1048583, 0.05, 1.0, 1024, 0.1),
+    "C2": _c("C2", 2, 8, None, 0.05, 1.0, 512, 0.08, rank=2, moduli=(4096, 4096),
+             gen=[[1, 3, 5, 7, 9, 11, 13, 15], [0, 1, 3, 5, 7, 9, 11, 13]]),
+    "C3": _c("C3", 3, 6, 262147, 0.05, 0.5, 512, 0.1, batch=512, c_range=(0.3, 0.7), p_max=3),
+    "C4": _c("C4", 4, 20, 1073741827, 0.02, 0.1, 64, 0.15),
+}
+
+
+def generating_vector(cfg: Config, recompute: bool = False):
+    cat = _catalog()
+    if not recompute and cfg.name in cat:
+        return cat[cfg.name]["z"]
+    z, _ = cbc_construct(cfg.N, cfg.d)
+    return [int(x) for x in z]
+
+
+def lattice(cfg: Config, recompute: bool = False) -> Lattice:
+    if cfg.rank == 2:
+        return Lattice.create(cfg.d, 2, cfg.gen, cfg.moduli)
+    return Lattice.rank1(generating_vector(cfg, recompute), cfg.N)
+
+
+def problem(cfg: Config, batch: int | None = None):
+    """(a, b, c[batch,d], p[batch,d]) from the seed schedule."""
+    batch = cfg.batch if batch is None else batch
+    a, b, c, p = problem_draw(cfg.seed, cfg.d, cfg.batch, cfg.c_range[0], cfg.c_range[1], cfg.p_max)
+    return a, b, c[:batch], p[:batch]
+
+
+def small_rank1(d: int, n: int, eps=0.1, sigma=0.1, seed=7, batch=1, c_range=(0.4, 0.6), p_max=2):
+    """Test-size rank-1 problem: CBC lattice + seeded families."""
+    z, _ = cbc_construct(n, d)
+    lat = Lattice.rank1(z, n)
+    a, b, c, p = problem_draw(seed, d, batch, c_range[0], c_range[1], p_max)
+    return lat, a, b, c, p

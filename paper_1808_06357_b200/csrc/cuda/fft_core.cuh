@@ -1,0 +1,249 @@
+// In-register small DFTs and the shared-memory Stockham stage used by the
+// fused Strang pass kernels (fft_pass.cuh).
+//
+// Everything here is __host__ __device__ so the exact same index algebra is
+// exercised by the CPU emulation test (tests/test_fft_core_emulation.py runs
+// the nvcc-built host harness csrc/cuda/fft_core_hosttest.cu).
+//
+// Conventions: complex fp64 is double2 (x = re, y = im). A transform of sign
+// SIGN computes X[k] = sum_n x[n] exp(SIGN * 2*pi*i*n*k/R); SIGN=-1 is the
+// forward DFT of SPEC.md:243-251 (analyze), SIGN=+1 the unnormalised inverse
+// (synthesize).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <utility>
+
+#include "dft_consts.h"
+
+#if defined(__CUDACC__)
+#define LD_HD __host__ __device__ __forceinline__
+#else
+#define LD_HD inline
+#endif
+
+namespace lattdse_dev {
+
+// ---------------------------------------------------------------- complex ops
+LD_HD double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+LD_HD double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+LD_HD double2 c_mul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+LD_HD double2 c_mulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+LD_HD double2 c_scale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// a * (i*S), S = +-1
+template <int S> LD_HD double2 c_muli(double2 a) {
+  return S > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+// ------------------------------------------------------- compile-time loops
+template <class F, int... Is>
+LD_HD void sfor_impl(F&& f, std::integer_sequence<int, Is...>) {
+  (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, class F> LD_HD void sfor(F&& f) {
+  sfor_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+// multiply by the compile-time root exp(SIGN*2*pi*i*M/R)
+template <int R, int M, int SIGN> LD_HD double2 tw_const(double2 a) {
+  constexpr int m = ((M % R) + R) % R;
+  if constexpr (m == 0) {
+    return a;
+  } else if constexpr (2 * m == R) {
+    return make_double2(-a.x, -a.y);
+  } else if constexpr (4 * m == R) {
+    return c_muli<SIGN>(a);
+  } else if constexpr (4 * m == 3 * R) {
+    return c_muli<-SIGN>(a);
+  } else {
+    constexpr double c = TwC<R, m>::c;
+    constexpr double s = SIGN * TwC<R, m>::s;
+    return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
+  }
+}
+
+// ----------------------------------------------------------- small DFTs
+template <int R, int SIGN> struct DFT;
+
+template <int SIGN> struct DFT<1, SIGN> {
+  LD_HD static void run(double2*) {}
+};
+
+template <int SIGN> struct DFT<2, SIGN> {
+  LD_HD static void run(double2* x) {
+    double2 t = x[0];
+    x[0] = c_add(t, x[1]);
+    x[1] = c_sub(t, x[1]);
+  }
+};
+
+template <int SIGN> struct DFT<3, SIGN> {
+  LD_HD static void run(double2* x) {
+    constexpr double h = TwC<3, 1>::s;  // sqrt(3)/2
+    double2 s = c_add(x[1], x[2]);
+    double2 d = c_sub(x[1], x[2]);
+    double2 m = make_double2(fma(-0.5, s.x, x[0].x), fma(-0.5, s.y, x[0].y));
+    x[0] = c_add(x[0], s);
+    double2 u = c_muli<SIGN>(c_scale(d, h));  // i*SIGN*h*(x1-x2)
+    x[1] = c_add(m, u);
+    x[2] = c_sub(m, u);
+  }
+};
+
+template <int SIGN> struct DFT<4, SIGN> {
+  LD_HD static void run(double2* x) {
+    double2 a = c_add(x[0], x[2]);
+    double2 b = c_sub(x[0], x[2]);
+    double2 c = c_add(x[1], x[3]);
+    double2 d = c_muli<SIGN>(c_sub(x[1], x[3]));
+    x[0] = c_add(a, c);
+    x[2] = c_sub(a, c);
+    x[1] = c_add(b, d);
+    x[3] = c_sub(b, d);
+  }
+};
+
+template <int SIGN> struct DFT<5, SIGN> {
+  LD_HD static void run(double2* x) {
+    constexpr double c1 = TwC<5, 1>::c, c2 = TwC<5, 2>::c;
+    constexpr double s1 = TwC<5, 1>::s, s2 = TwC<5, 2>::s;
+    double2 t1 = c_add(x[1], x[4]), t2 = c_add(x[2], x[3]);
+    double2 t3 = c_sub(x[1], x[4]), t4 = c_sub(x[2], x[3]);
+    double2 x0 = x[0];
+    x[0] = c_add(x0, c_add(t1, t2));
+    double2 a1 = make_double2(fma(c2, t2.x, fma(c1, t1.x, x0.x)), fma(c2, t2.y, fma(c1, t1.y, x0.y)));
+    double2 a2 = make_double2(fma(c1, t2.x, fma(c2, t1.x, x0.x)), fma(c1, t2.y, fma(c2, t1.y, x0.y)));
+    double2 b1 = make_double2(fma(s2, t4.x, s1 * t3.x), fma(s2, t4.y, s1 * t3.y));
+    double2 b2 = make_double2(fma(-s1, t4.x, s2 * t3.x), fma(-s1, t4.y, s2 * t3.y));
+    b1 = c_muli<SIGN>(b1);
+    b2 = c_muli<SIGN>(b2);
+    x[1] = c_add(a1, b1);
+    x[4] = c_sub(a1, b1);
+    x[2] = c_add(a2, b2);
+    x[3] = c_sub(a2, b2);
+  }
+};
+
+// Cooley-Tukey R = R1*R2 with constant inner twiddles.
+// input n = R2*n1 + n2, output k = k1 + R1*k2.
+template <int R1, int R2, int SIGN> struct DFT_CT {
+  LD_HD static void run(double2* x) {
+    constexpr int R = R1 * R2;
+    double2 y[R];
+    sfor<R2>([&](auto n2c) {
+      constexpr int n2 = decltype(n2c)::value;
+      double2 t[R1];
+      sfor<R1>([&](auto n1c) { t[decltype(n1c)::value] = x[R2 * decltype(n1c)::value + n2]; });
+      DFT<R1, SIGN>::run(t);
+      sfor<R1>([&](auto k1c) {
+        constexpr int k1 = decltype(k1c)::value;
+        y[n2 * R1 + k1] = tw_const<R, n2 * k1, SIGN>(t[k1]);
+      });
+    });
+    sfor<R1>([&](auto k1c) {
+      constexpr int k1 = decltype(k1c)::value;
+      double2 t[R2];
+      sfor<R2>([&](auto n2c) { t[decltype(n2c)::value] = y[decltype(n2c)::value * R1 + k1]; });
+      DFT<R2, SIGN>::run(t);
+      sfor<R2>([&](auto k2c) { x[k1 + R1 * decltype(k2c)::value] = t[decltype(k2c)::value]; });
+    });
+  }
+};
+
+constexpr int crt_index(int k1, int k2, int R1, int R2) {
+  for (int k = 0; k < R1 * R2; ++k)
+    if (k % R1 == k1 && k % R2 == k2) return k;
+  return -1;
+}
+
+// Good-Thomas prime-factor R = R1*R2, gcd(R1,R2)=1: no twiddles.
+// input n = (R2*n1 + R1*n2) mod R, output k = CRT(k1, k2).
+template <int R1, int R2, int SIGN> struct DFT_PFA {
+  LD_HD static void run(double2* x) {
+    constexpr int R = R1 * R2;
+    double2 y[R];
+    sfor<R2>([&](auto n2c) {
+      constexpr int n2 = decltype(n2c)::value;
+      double2 t[R1];
+      sfor<R1>([&](auto n1c) {
+        constexpr int n1 = decltype(n1c)::value;
+        t[n1] = x[(R2 * n1 + R1 * n2) % R];
+      });
+      DFT<R1, SIGN>::run(t);
+      sfor<R1>([&](auto k1c) { y[n2 * R1 + decltype(k1c)::value] = t[decltype(k1c)::value]; });
+    });
+    sfor<R1>([&](auto k1c) {
+      constexpr int k1 = decltype(k1c)::value;
+      double2 t[R2];
+      sfor<R2>([&](auto n2c) { t[decltype(n2c)::value] = y[decltype(n2c)::value * R1 + k1]; });
+      DFT<R2, SIGN>::run(t);
+      sfor<R2>([&](auto k2c) {
+        constexpr int k2 = decltype(k2c)::value;
+        x[crt_index(k1, k2, R1, R2)] = t[k2];
+      });
+    });
+  }
+};
+
+template <int SIGN> struct DFT<6, SIGN> : DFT_PFA<2, 3, SIGN> {};
+template <int SIGN> struct DFT<8, SIGN> : DFT_CT<2, 4, SIGN> {};
+template <int SIGN> struct DFT<9, SIGN> : DFT_CT<3, 3, SIGN> {};
+template <int SIGN> struct DFT<10, SIGN> : DFT_PFA<2, 5, SIGN> {};
+template <int SIGN> struct DFT<12, SIGN> : DFT_PFA<3, 4, SIGN> {};
+template <int SIGN> struct DFT<15, SIGN> : DFT_PFA<3, 5, SIGN> {};
+template <int SIGN> struct DFT<16, SIGN> : DFT_CT<4, 4, SIGN> {};
+template <int SIGN> struct DFT<18, SIGN> : DFT_PFA<2, 9, SIGN> {};
+template <int SIGN> struct DFT<20, SIGN> : DFT_PFA<4, 5, SIGN> {};
+template <int SIGN> struct DFT<24, SIGN> : DFT_PFA<3, 8, SIGN> {};
+template <int SIGN> struct DFT<27, SIGN> : DFT_CT<3, 9, SIGN> {};
+template <int SIGN> struct DFT<32, SIGN> : DFT_CT<4, 8, SIGN> {};
+
+// ------------------------------------------------------------ radix plan
+// Greedy factorisation of a transform length into in-register radices.
+constexpr int kRadixPref[] = {16, 15, 12, 9, 10, 8, 6, 5, 4, 3, 2};
+
+constexpr int pick_radix(int rem) {
+  for (int r : kRadixPref)
+    if (rem % r == 0) return r;
+  return rem;  // rejected by the static_assert in Plan
+}
+
+template <int L> struct Plan {
+  static constexpr int count() {
+    int n = 0, rem = L;
+    while (rem > 1) {
+      rem /= pick_radix(rem);
+      ++n;
+    }
+    return n;
+  }
+  static constexpr int nst = count();
+  static constexpr int radix(int s) {
+    int rem = L;
+    for (int i = 0; i < s; ++i) rem /= pick_radix(rem);
+    return pick_radix(rem);
+  }
+  // Ns = product of the radices of the earlier stages
+  static constexpr int ns(int s) {
+    int p = 1;
+    for (int i = 0; i < s; ++i) p *= radix(i);
+    return p;
+  }
+  static constexpr bool valid() {
+    for (int s = 0; s < nst; ++s) {
+      int r = radix(s);
+      if (r > 32) return false;
+    }
+    return L >= 2;
+  }
+  static_assert(valid(), "transform length must factor into radices <= 32 from kRadixPref");
+};
+
+}  // namespace lattdse_dev

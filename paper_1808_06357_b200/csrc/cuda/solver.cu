@@ -1,0 +1,847 @@
+// Device orchestration of the Strang hot path on one B200.
+//
+// State between calls: samples u(p_kappa) in kappa order, one N-vector per
+// ensemble member. A step(n) call runs entirely on the
+// device stream with no host synchronisation until it returns:
+//
+//   rank-1, method "circulant" (default): F^-1 D F is the circulant matrix of
+//     k = F^-1(D)/N, applied as a length-M cyclic convolution (M >= 2N-1,
+//     M = M1*M2) through a four-step FFT, so one step is
+//        ROW pass  : FFT_M2 . (x K^) . IFFT_M2
+//        COL pass  : IFFT_M1 . (mask j<N, x V) . FFT_M1   (with 4-step twiddles)
+//     and the two potential half steps of consecutive steps are fused into V.
+//   rank-1, method "bluestein": the literal two length-N DFTs per step
+//     (Algorithm 1), each a Bluestein convolution: 4 passes.
+//   rank-2 grid: ROW pass IFFT.(xV).FFT along n2, COL pass FFT.(xD/N).IFFT
+//     along n1.
+//
+// Ensemble members are stepped in groups sized to stay L2-resident for the
+// whole step(n) call (each member's work buffer is reused across steps).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+
+#include "fft_pass.cuh"
+#include "lattdse/solver.hpp"
+#include "pass_registry.hpp"
+
+using namespace lattdse_dev;
+
+namespace lattdse {
+
+#define LD_CK(x)                                                                                      \
+  do {                                                                                                \
+    cudaError_t e_ = (x);                                                                             \
+    if (e_ != cudaSuccess) raise(Errc::device_error, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ------------------------------------------------------------- registry
+namespace dev {
+namespace {
+struct Registry {
+  std::mutex mu;
+  std::map<std::tuple<int, int, int, int>, PassKernel> k;
+};
+Registry& registry() {
+  static Registry r;
+  return r;
+}
+}  // namespace
+
+PassKernel* find_pass_kernel(int axis, int L, int prog, int sign) {
+  auto& r = registry();
+  std::lock_guard<std::mutex> g(r.mu);
+  auto it = r.k.find({axis, L, prog, sign});
+  return it == r.k.end() ? nullptr : &it->second;
+}
+void register_pass_kernel(int axis, int L, int prog, int sign, const PassKernel& k) {
+  auto& r = registry();
+  std::lock_guard<std::mutex> g(r.mu);
+  r.k[{axis, L, prog, sign}] = k;
+}
+std::vector<int> pass_lengths(int axis) {
+  auto& r = registry();
+  std::lock_guard<std::mutex> g(r.mu);
+  std::vector<int> out;
+  for (auto& [key, v] : r.k)
+    if (std::get<0>(key) == axis && std::get<2>(key) == PROG_DOUBLE && std::get<3>(key) == -1)
+      out.push_back(std::get<1>(key));
+  return out;
+}
+}  // namespace dev
+
+// --------------------------------------------------------- aux kernels
+namespace {
+
+__global__ void k_phase(const double* __restrict__ v, long long n, double coef, double2* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double s, c;
+    sincos(coef * v[i], &s, &c);
+    out[i] = make_double2(c, s);
+  }
+}
+
+// c_j = exp(-pi i j^2 / N), j^2 reduced mod 2N exactly; also conj(c) and c/N.
+__global__ void k_chirp(long long N, double2* __restrict__ c, double2* __restrict__ cc, double2* __restrict__ cn) {
+  const double invN = 1.0 / (double)N;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
+    unsigned long long q = (unsigned long long)(((unsigned __int128)j * (unsigned __int128)j) % (unsigned __int128)(2 * N));
+    double sgn = 1.0;
+    if (q >= (unsigned long long)N) {  // exp(-pi i (q)/N) = -exp(-pi i (q-N)/N)
+      q -= (unsigned long long)N;
+      sgn = -1.0;
+    }
+    double s, co;
+    sincospi((double)q / (double)N, &s, &co);
+    double2 v = make_double2(sgn * co, -sgn * s);
+    c[j] = v;
+    cc[j] = make_double2(v.x, -v.y);
+    cn[j] = make_double2(v.x * invN, v.y * invN);
+  }
+}
+
+// Embed a length-N sequence into a length-M cyclic kernel, scaled:
+//  periodic: K[t] = k[t mod N] for t in (-N, N)   (circulant kernel)
+//  even:     K[t] = k[|t|]      for t in (-N, N)   (Bluestein chirp)
+__global__ void k_wrap(const double2* __restrict__ k, long long N, long long M, double scale, int even,
+                       double2* __restrict__ K) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < M; t += (long long)gridDim.x * blockDim.x) {
+    double2 v = make_double2(0.0, 0.0);
+    if (t < N)
+      v = k[t];
+    else if (t > M - N)
+      v = even ? k[M - t] : k[t - (M - N)];
+    K[t] = make_double2(v.x * scale, v.y * scale);
+  }
+}
+
+__global__ void k_lut_gather(const unsigned short* __restrict__ idx, const double2* __restrict__ lut, long long n,
+                             double2* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = lut[idx[i]];
+}
+
+__global__ void k_mul(const double2* __restrict__ a, const double2* __restrict__ b, long long n, double2* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = c_mul(a[i], b[i]);
+}
+
+// Per-block partial sums of w_i * |x_i|^2 (w from a real table, an index
+// table scaled, or 1), batch along blockIdx.y.
+__global__ void k_wsumsq(const double2* __restrict__ x, long long n, long long bstride, const double* __restrict__ w,
+                         const unsigned short* __restrict__ widx, double wscale, const double2* __restrict__ y,
+                         double* __restrict__ partial) {
+  __shared__ double red[32];
+  const double2* xb = x + blockIdx.y * bstride;
+  const double2* yb = y ? y + blockIdx.y * bstride : nullptr;
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double2 v = xb[i];
+    if (yb) v = c_sub(v, yb[i]);
+    double m = v.x * v.x + v.y * v.y;
+    if (w) m *= w[i];
+    if (widx) m *= wscale * (double)widx[i];
+    acc += m;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = acc;
+  }
+}
+
+template <class T> struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (p && n == count) return;
+    release();
+    if (count == 0) return;
+    LD_CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+};
+
+const long double kPiL = 3.141592653589793238462643383279502884L;
+
+std::vector<double2> root_table(long long n, long long count, long long stride) {
+  std::vector<double2> t(count);
+  for (long long i = 0; i < count; ++i) {
+    long long q = (i * stride) % n;
+    long double a = -2.0L * kPiL * (long double)q / (long double)n;
+    t[i] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  return t;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- Impl
+struct Solver::Impl {
+  // problem
+  int rank = 1, dim = 1;
+  long long N = 0, n1 = 0, n2 = 0;  // rank-2: grid n1 x n2
+  long long batch = 1, group = 1;
+  double eps = 1, dt_ = 0;
+  bool have_dt = false;
+  std::string method;
+  ProblemSpec prob;
+  Lattice lat;
+  std::uint32_t max_norm2 = 0;
+
+  // transform geometry
+  long long M = 0, M1 = 0, M2 = 0;  // work = M1 rows x M2 cols
+  int tw_shift = 0;
+
+  // device
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  DBuf<double2> work, samples, coef, tmp;
+  DBuf<double> v;                 // potential at the points
+  DBuf<unsigned short> nidx;      // ||h_chi||^2 per chi
+  DBuf<double2> V, Vh, Ventry, Vexit, kin_lut, kin_full;
+  DBuf<double2> Khat, B1hat, B2hat, chirp, chirp_c, chirp_n;
+  DBuf<double2> tw_col, tw_row, tw_lo, tw_hi, scal;
+  DBuf<double> partial;
+  DBuf<char> flush;
+  bool bluestein_tables = false;
+  long long launches = 0;
+
+  explicit Impl(const Lattice& l) : lat(l) {}
+
+  // ---- launch helpers
+  void launch_pass(int axis, int L, int prog, int sign, PassArgs a, long long nlines, long long nbatch) {
+    dev::PassKernel* k = dev::find_pass_kernel(axis, L, prog, sign);
+    if (!k) raise(Errc::unsupported, "no pass kernel compiled for axis " + std::to_string(axis) + " L=" + std::to_string(L));
+    if (!k->attr_set) {
+      LD_CK(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem));
+      k->attr_set = true;
+    }
+    a.nlines = (int)nlines;
+    dim3 grid((unsigned)((nlines + k->B - 1) / k->B), (unsigned)nbatch);
+    void* args[] = {&a};
+    LD_CK(cudaLaunchKernel(k->fn, grid, dim3(k->NT), args, (size_t)k->smem, stream));
+    ++launches;
+  }
+  int grid1d(long long n) const { return (int)std::min<long long>((n + 255) / 256, 148 * 16); }
+  void aux_done() {
+    LD_CK(cudaGetLastError());
+    ++launches;
+  }
+
+  PassArgs base_args(int axis) const {
+    PassArgs a{};
+    a.tw_shift = tw_shift;
+    a.tw_lo = tw_lo.p;
+    a.tw_hi = tw_hi.p;
+    a.fft_tw = axis == AX_COL ? tw_col.p : tw_row.p;
+    a.ncols = (int)M2;
+    return a;
+  }
+  static void set_diag(PassArgs& a, const double2* d) {
+    a.diag_kind = d ? DG_CPLX : DG_NONE;
+    a.diag = d;
+  }
+
+  // ---- rank-1 four-step passes (COL length M1, ROW length M2)
+  // entry: compact[j<N] x diag -> FFT_M1 -> twiddle -> work
+  void r1_col_entry(const double2* in, long long in_stride, const double2* diag, double2* w, long long nb) {
+    PassArgs a = base_args(AX_COL);
+    a.in = in;
+    a.out = w;
+    a.in_bstride = in_stride;
+    a.out_bstride = M;
+    a.nvalid_in = N;
+    a.nvalid_mid = a.nvalid_out = M;
+    a.post_tw = 1;
+    set_diag(a, diag);
+    launch_pass(AX_COL, (int)M1, PROG_LOADDIAG, -1, a, M2, nb);
+  }
+  void r1_col_mid(double2* w, const double2* diag, long long nb) {
+    PassArgs a = base_args(AX_COL);
+    a.in = w;
+    a.out = w;
+    a.in_bstride = a.out_bstride = M;
+    a.nvalid_in = a.nvalid_out = M;
+    a.nvalid_mid = N;
+    a.pre_tw = a.post_tw = 1;
+    set_diag(a, diag);
+    launch_pass(AX_COL, (int)M1, PROG_DOUBLE, +1, a, M2, nb);
+  }
+  void r1_col_mid_lut(double2* w, long long nb) {  // x D/N through the norm index
+    PassArgs a = base_args(AX_COL);
+    a.in = w;
+    a.out = w;
+    a.in_bstride = a.out_bstride = M;
+    a.nvalid_in = a.nvalid_out = M;
+    a.nvalid_mid = N;
+    a.pre_tw = a.post_tw = 1;
+    a.diag_kind = DG_LUT16;
+    a.diag_idx = nidx.p;
+    a.lut = kin_lut.p;
+    launch_pass(AX_COL, (int)M1, PROG_DOUBLE, +1, a, M2, nb);
+  }
+  void r1_col_exit(double2* w, const double2* diag, double2* out, long long out_stride, long long nb) {
+    PassArgs a = base_args(AX_COL);
+    a.in = w;
+    a.out = out;
+    a.in_bstride = M;
+    a.out_bstride = out_stride;
+    a.nvalid_in = a.nvalid_mid = M;
+    a.nvalid_out = N;
+    a.pre_tw = 1;
+    set_diag(a, diag);
+    launch_pass(AX_COL, (int)M1, PROG_STOREDIAG, +1, a, M2, nb);
+  }
+  void r1_row_mid(double2* w, const double2* table, long long nb) {
+    PassArgs a = base_args(AX_ROW);
+    a.in = w;
+    a.out = w;
+    a.in_bstride = a.out_bstride = M;
+    a.nvalid_in = a.nvalid_mid = a.nvalid_out = M;
+    set_diag(a, table);
+    launch_pass(AX_ROW, (int)M2, PROG_DOUBLE, -1, a, M1, nb);
+  }
+  void r1_row_fwd(double2* w) {
+    PassArgs a = base_args(AX_ROW);
+    a.in = w;
+    a.out = w;
+    a.in_bstride = a.out_bstride = M;
+    a.nvalid_in = a.nvalid_mid = a.nvalid_out = M;
+    launch_pass(AX_ROW, (int)M2, PROG_LOADDIAG, -1, a, M1, 1);
+  }
+  // ---- rank-2 passes (ROW length n2 over n1 rows; COL length n1 over n2 cols)
+  void g_row(int prog, int sign, const double2* in, double2* out, const double2* diag, long long nb) {
+    PassArgs a = base_args(AX_ROW);
+    a.in = in;
+    a.out = out;
+    a.in_bstride = a.out_bstride = N;
+    a.nvalid_in = a.nvalid_mid = a.nvalid_out = N;
+    set_diag(a, diag);
+    launch_pass(AX_ROW, (int)n2, prog, sign, a, n1, nb);
+  }
+  void g_col(int prog, int sign, const double2* in, double2* out, int dkind, long long nb) {
+    PassArgs a = base_args(AX_COL);
+    a.in = in;
+    a.out = out;
+    a.in_bstride = a.out_bstride = N;
+    a.nvalid_in = a.nvalid_mid = a.nvalid_out = N;
+    a.diag_kind = dkind;
+    a.diag_idx = nidx.p;
+    a.lut = dkind == DG_SCALAR ? scal.p : kin_lut.p;
+    launch_pass(AX_COL, (int)n1, prog, sign, a, n2, nb);
+  }
+
+  // ---- setup
+  void choose_geometry() {
+    if (rank == 2) {
+      M1 = n1;
+      M2 = n2;
+      M = N;
+      if (!dev::find_pass_kernel(AX_ROW, (int)n2, PROG_DOUBLE, -1) || !dev::find_pass_kernel(AX_COL, (int)n1, PROG_DOUBLE, -1))
+        raise(Errc::unsupported, "rank-2 grid " + std::to_string(n1) + "x" + std::to_string(n2) + " has no compiled pass kernels");
+      return;
+    }
+    const long long need = 2 * N - 1;
+    long long best = -1, b1 = 0, b2 = 0;
+    double bal = 0;
+    for (int L1 : dev::pass_lengths(AX_COL))
+      for (int L2 : dev::pass_lengths(AX_ROW)) {
+        long long m = (long long)L1 * L2;
+        if (m < need) continue;
+        double bl = std::fabs(std::log((double)L1 / L2));
+        if (best < 0 || m < best || (m == best && (bl < bal - 1e-12 || (std::fabs(bl - bal) <= 1e-12 && L1 < b1)))) {
+          best = m;
+          b1 = L1;
+          b2 = L2;
+          bal = bl;
+        }
+      }
+    if (best < 0) raise(Errc::unsupported, "N=" + std::to_string(N) + " exceeds the single-level four-step range");
+    M = best;
+    M1 = b1;
+    M2 = b2;
+  }
+
+  void upload_twiddles() {
+    auto up = [&](DBuf<double2>& b, const std::vector<double2>& h) {
+      b.alloc(h.size());
+      LD_CK(cudaMemcpyAsync(b.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
+    };
+    up(tw_col, root_table(M1, M1, 1));
+    up(tw_row, root_table(M2, M2, 1));
+    tw_shift = 0;
+    while ((1LL << (2 * tw_shift)) < M) ++tw_shift;
+    const long long nlo = 1LL << tw_shift, nhi = (M + nlo - 1) / nlo;
+    up(tw_lo, root_table(M, nlo, 1));
+    up(tw_hi, root_table(M, nhi, nlo));
+    std::vector<double2> s = {make_double2(1.0 / (double)N, 0.0)};
+    up(scal, s);
+    LD_CK(cudaStreamSynchronize(stream));
+  }
+
+  void build_chirp_tables() {
+    if (bluestein_tables || rank != 1) return;
+    chirp.alloc(N);
+    chirp_c.alloc(N);
+    chirp_n.alloc(N);
+    k_chirp<<<grid1d(N), 256, 0, stream>>>(N, chirp.p, chirp_c.p, chirp_n.p);
+    aux_done();
+    // B1 = FFT_M(wrap conj c)/M (forward DFT), B2 = FFT_M(wrap c)/M (inverse)
+    B1hat.alloc(M);
+    B2hat.alloc(M);
+    k_wrap<<<grid1d(M), 256, 0, stream>>>(chirp_c.p, N, M, 1.0 / (double)M, 1, B1hat.p);
+    aux_done();
+    r1_fft_table_full(B1hat.p);
+    k_wrap<<<grid1d(M), 256, 0, stream>>>(chirp.p, N, M, 1.0 / (double)M, 1, B2hat.p);
+    aux_done();
+    r1_fft_table_full(B2hat.p);
+    bluestein_tables = true;
+  }
+  void r1_fft_table_full(double2* w) {
+    PassArgs a = base_args(AX_COL);
+    a.in = w;
+    a.out = w;
+    a.in_bstride = a.out_bstride = M;
+    a.nvalid_in = a.nvalid_mid = a.nvalid_out = M;
+    a.post_tw = 1;
+    launch_pass(AX_COL, (int)M1, PROG_LOADDIAG, -1, a, M2, 1);
+    r1_row_fwd(w);
+  }
+
+  // samples (N, one member) -> coefficients (N) and back, on the device
+  void analyze_dev(const double2* s, double2* c, double2* w) {
+    if (rank == 1) {
+      build_chirp_tables();
+      r1_col_entry(s, N, chirp.p, w, 1);
+      r1_row_mid(w, B1hat.p, 1);
+      r1_col_exit(w, chirp_n.p, c, N, 1);
+    } else {
+      g_row(PROG_LOADDIAG, -1, s, w, nullptr, 1);
+      g_col(PROG_STOREDIAG, -1, w, c, DG_SCALAR, 1);
+    }
+  }
+  void synthesize_dev(const double2* c, double2* s, double2* w) {
+    if (rank == 1) {
+      build_chirp_tables();
+      r1_col_entry(c, N, chirp_c.p, w, 1);
+      r1_row_mid(w, B2hat.p, 1);
+      r1_col_exit(w, chirp_c.p, s, N, 1);
+    } else {
+      g_col(PROG_LOADDIAG, +1, c, w, DG_NONE, 1);
+      g_row(PROG_STOREDIAG, +1, w, s, nullptr, 1);
+    }
+  }
+
+  void build_propagator(double dt) {
+    // potential phases: V = exp(-i dt v / eps), Vh = exp(-i dt v / (2 eps))
+    V.alloc(N);
+    Vh.alloc(N);
+    k_phase<<<grid1d(N), 256, 0, stream>>>(v.p, N, -dt / eps, V.p);
+    aux_done();
+    k_phase<<<grid1d(N), 256, 0, stream>>>(v.p, N, -dt / (2.0 * eps), Vh.p);
+    aux_done();
+    // kinetic LUT exp(-i eps dt 2 pi^2 s)/N for s = 0..max ||h||^2
+    std::vector<double2> lut(max_norm2 + 1);
+    for (std::uint32_t s = 0; s <= max_norm2; ++s) {
+      long double a = -(long double)eps * (long double)dt * 2.0L * kPiL * kPiL * (long double)s;
+      long double r = fmodl(a, 2.0L * kPiL);
+      lut[s] = make_double2((double)(cosl(r) / (long double)N), (double)(sinl(r) / (long double)N));
+    }
+    kin_lut.alloc(lut.size());
+    LD_CK(cudaMemcpyAsync(kin_lut.p, lut.data(), lut.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
+    LD_CK(cudaStreamSynchronize(stream));  // lut is a host temporary
+
+    if (rank == 1) {
+      build_chirp_tables();
+      if (method == "circulant") {
+        // k = F^-1(D)/N: synthesize the D/N phases (Bluestein on the device),
+        // wrap periodically into length M, K^ = FFT_M(K)/M.
+        kin_full.alloc(N);
+        k_lut_gather<<<grid1d(N), 256, 0, stream>>>(nidx.p, kin_lut.p, N, kin_full.p);
+        aux_done();
+        tmp.alloc(std::max<long long>(N, 1));
+        DBuf<double2> scratch;
+        scratch.alloc(M);
+        synthesize_dev(kin_full.p, tmp.p, scratch.p);
+        Khat.alloc(M);
+        k_wrap<<<grid1d(M), 256, 0, stream>>>(tmp.p, N, M, 1.0 / (double)M, 0, Khat.p);
+        aux_done();
+        r1_fft_table_full(Khat.p);
+        LD_CK(cudaStreamSynchronize(stream));
+        kin_full.release();
+        Ventry.release();
+        Vexit.release();
+      } else {
+        Ventry.alloc(N);
+        Vexit.alloc(N);
+        k_mul<<<grid1d(N), 256, 0, stream>>>(Vh.p, chirp.p, N, Ventry.p);
+        aux_done();
+        k_mul<<<grid1d(N), 256, 0, stream>>>(Vh.p, chirp_c.p, N, Vexit.p);
+        aux_done();
+      }
+    }
+    LD_CK(cudaStreamSynchronize(stream));
+    dt_ = dt;
+    have_dt = true;
+  }
+
+  // ---- stepping (asynchronous on `stream`); optional per-pass events
+  struct PassTimer {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> col, row;
+  };
+  template <class F> void timed(PassTimer* pt, bool is_col, F&& f) {
+    if (!pt) {
+      f();
+      return;
+    }
+    cudaEvent_t a, b;
+    LD_CK(cudaEventCreate(&a));
+    LD_CK(cudaEventCreate(&b));
+    LD_CK(cudaEventRecord(a, stream));
+    f();
+    LD_CK(cudaEventRecord(b, stream));
+    (is_col ? pt->col : pt->row).push_back({a, b});
+  }
+
+  void enqueue_steps(long long nsteps, PassTimer* pt = nullptr) {
+    if (!have_dt) raise(Errc::config_error, "set_dt must be called before stepping");
+    if (nsteps <= 0) return;
+    for (long long g0 = 0; g0 < batch; g0 += group) {
+      const long long gb = std::min(group, batch - g0);
+      double2* s = samples.p + g0 * N;
+      double2* w = work.p;
+      if (rank == 2) {
+        timed(pt, false, [&] { g_row(PROG_LOADDIAG, -1, s, w, Vh.p, gb); });
+        for (long long k = 0; k < nsteps; ++k) {
+          timed(pt, true, [&] { g_col(PROG_DOUBLE, -1, w, w, DG_LUT16, gb); });
+          if (k + 1 < nsteps)
+            timed(pt, false, [&] { g_row(PROG_DOUBLE, +1, w, w, V.p, gb); });
+          else
+            timed(pt, false, [&] { g_row(PROG_STOREDIAG, +1, w, s, Vh.p, gb); });
+        }
+      } else if (method == "circulant") {
+        timed(pt, true, [&] { r1_col_entry(s, N, Vh.p, w, gb); });
+        for (long long k = 0; k < nsteps; ++k) {
+          timed(pt, false, [&] { r1_row_mid(w, Khat.p, gb); });
+          if (k + 1 < nsteps)
+            timed(pt, true, [&] { r1_col_mid(w, V.p, gb); });
+          else
+            timed(pt, true, [&] { r1_col_exit(w, Vh.p, s, N, gb); });
+        }
+      } else {  // literal Bluestein: two length-N DFTs per step
+        timed(pt, true, [&] { r1_col_entry(s, N, Ventry.p, w, gb); });
+        for (long long k = 0; k < nsteps; ++k) {
+          timed(pt, false, [&] { r1_row_mid(w, B1hat.p, gb); });
+          timed(pt, true, [&] { r1_col_mid_lut(w, gb); });
+          timed(pt, false, [&] { r1_row_mid(w, B2hat.p, gb); });
+          if (k + 1 < nsteps)
+            timed(pt, true, [&] { r1_col_mid(w, V.p, gb); });
+          else
+            timed(pt, true, [&] { r1_col_exit(w, Vexit.p, s, N, gb); });
+        }
+      }
+    }
+  }
+
+  std::vector<double> reduce(const double2* x, long long n, long long nb, long long bstride, const double* w,
+                             const unsigned short* widx, double wscale, const double2* y) {
+    const int blocks = (int)std::min<long long>((n + 255) / 256, 592);
+    partial.alloc((size_t)blocks * nb);
+    k_wsumsq<<<dim3(blocks, (unsigned)nb), 256, 0, stream>>>(x, n, bstride, w, widx, wscale, y, partial.p);
+    aux_done();
+    std::vector<double> h((size_t)blocks * nb);
+    LD_CK(cudaMemcpyAsync(h.data(), partial.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    LD_CK(cudaStreamSynchronize(stream));
+    std::vector<double> out(nb);
+    for (long long b = 0; b < nb; ++b) {
+      long double s = 0;
+      for (int i = 0; i < blocks; ++i) s += h[b * blocks + i];
+      out[b] = (double)s;
+    }
+    return out;
+  }
+};
+
+// ------------------------------------------------------------ Solver
+Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& prob, const SolverOptions& opt)
+    : p_(std::make_unique<Impl>(lat)) {
+  Impl& s = *p_;
+  s.rank = lat.rank();
+  s.dim = lat.dim();
+  s.N = lat.n_total();
+  if (s.rank > 2) raise(Errc::unsupported, "the device path supports rank-1 and rank-2 lattices");
+  if (s.rank == 2) {
+    s.n1 = lat.moduli()[0];
+    s.n2 = lat.moduli()[1];
+  }
+  if (aa.n_total != s.N) raise(Errc::spec_mismatch, "anti-aliasing set does not match the lattice");
+  if (aa.max_norm2 > 65535) raise(Errc::unsupported, "||h||^2 above 65535 does not fit the uint16 norm index");
+  if (prob.initial.empty()) raise(Errc::invalid_argument, "problem needs at least one initial condition");
+  if (!(prob.eps > 0)) raise(Errc::invalid_argument, "eps must be > 0");
+  if ((int)prob.potential.a.size() != s.dim || (int)prob.potential.b.size() != std::max(0, s.dim - 1))
+    raise(Errc::invalid_argument, "potential coefficients do not match the dimension");
+  s.prob = prob;
+  s.eps = prob.eps;
+  s.batch = (long long)prob.initial.size();
+  s.method = s.rank == 2 ? "grid" : opt.method;
+  if (s.rank == 1 && s.method != "circulant" && s.method != "bluestein")
+    raise(Errc::invalid_argument, "method must be 'circulant' or 'bluestein'");
+  s.max_norm2 = aa.max_norm2;
+  s.device = opt.device;
+  LD_CK(cudaSetDevice(s.device));
+  LD_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+  s.choose_geometry();
+
+  // L2-resident ensemble groups: work buffers of the group + shared tables
+  // within ~70% of L2.
+  if (opt.group > 0) {
+    s.group = std::min<long long>(opt.group, s.batch);
+  } else {
+    int l2 = 0;
+    LD_CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s.device));
+    const double budget = 0.7 * l2 - 16.0 * (double)s.M - 16.0 * (double)s.N;
+    long long g = (long long)std::floor(budget / (16.0 * (double)s.M));
+    s.group = std::max<long long>(1, std::min<long long>(g, s.batch));
+    s.group = std::min<long long>(s.group, 65535);
+  }
+
+  s.upload_twiddles();
+  s.work.alloc((size_t)s.M * s.group);
+  s.samples.alloc((size_t)s.N * s.batch);
+  LD_CK(cudaMemsetAsync(s.samples.p, 0, sizeof(double2) * s.N * s.batch, s.stream));
+
+  // potential values and the norm index (host setup -> device, once)
+  auto vv = problems::sample_v(lat, prob.potential);
+  s.v.alloc(s.N);
+  LD_CK(cudaMemcpyAsync(s.v.p, vv.data(), sizeof(double) * s.N, cudaMemcpyHostToDevice, s.stream));
+  std::vector<unsigned short> ni(s.N);
+  for (long long c = 0; c < s.N; ++c) ni[c] = (unsigned short)aa.norm2[c];
+  s.nidx.alloc(s.N);
+  LD_CK(cudaMemcpyAsync(s.nidx.p, ni.data(), sizeof(unsigned short) * s.N, cudaMemcpyHostToDevice, s.stream));
+  LD_CK(cudaStreamSynchronize(s.stream));
+}
+
+Solver::~Solver() {
+  if (p_ && p_->stream) {
+    cudaStreamSynchronize(p_->stream);
+    cudaStreamDestroy(p_->stream);
+  }
+}
+
+void Solver::set_dt(double dt) {
+  if (!(dt != 0.0) || !std::isfinite(dt)) raise(Errc::invalid_argument, "dt must be finite and nonzero");
+  LD_CK(cudaSetDevice(p_->device));
+  p_->build_propagator(dt);
+}
+
+double Solver::dt() const { return p_->dt_; }
+
+void Solver::discretize_initial() {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  for (long long m = 0; m < s.batch; ++m) {
+    problems::Initial g = s.prob.initial[m];
+    auto gv = problems::sample_g(s.lat, g);
+    LD_CK(cudaMemcpy(s.samples.p + m * s.N, gv.data(), sizeof(double2) * s.N, cudaMemcpyHostToDevice));
+  }
+}
+
+void Solver::set_state(const std::complex<double>* data, std::int64_t count, Space space, std::int64_t m0) {
+  Impl& s = *p_;
+  if (m0 < 0 || count < 0 || m0 + count > s.batch) raise(Errc::invalid_argument, "set_state: member range out of bounds");
+  LD_CK(cudaSetDevice(s.device));
+  if (space == Space::samples) {
+    LD_CK(cudaMemcpyAsync(s.samples.p + m0 * s.N, data, sizeof(double2) * s.N * count, cudaMemcpyHostToDevice, s.stream));
+  } else {
+    s.coef.alloc(s.N);
+    for (std::int64_t m = 0; m < count; ++m) {
+      LD_CK(cudaMemcpyAsync(s.coef.p, data + m * s.N, sizeof(double2) * s.N, cudaMemcpyHostToDevice, s.stream));
+      s.synthesize_dev(s.coef.p, s.samples.p + (m0 + m) * s.N, s.work.p);
+    }
+  }
+  LD_CK(cudaStreamSynchronize(s.stream));
+}
+
+void Solver::get_state(std::complex<double>* data, std::int64_t count, Space space, std::int64_t m0) {
+  Impl& s = *p_;
+  if (m0 < 0 || count < 0 || m0 + count > s.batch) raise(Errc::invalid_argument, "get_state: member range out of bounds");
+  LD_CK(cudaSetDevice(s.device));
+  if (space == Space::samples) {
+    LD_CK(cudaMemcpyAsync(data, s.samples.p + m0 * s.N, sizeof(double2) * s.N * count, cudaMemcpyDeviceToHost, s.stream));
+  } else {
+    s.coef.alloc(s.N);
+    for (std::int64_t m = 0; m < count; ++m) {
+      s.analyze_dev(s.samples.p + (m0 + m) * s.N, s.coef.p, s.work.p);
+      LD_CK(cudaMemcpyAsync(data + m * s.N, s.coef.p, sizeof(double2) * s.N, cudaMemcpyDeviceToHost, s.stream));
+    }
+  }
+  LD_CK(cudaStreamSynchronize(s.stream));
+}
+
+void Solver::step(std::int64_t nsteps) {
+  LD_CK(cudaSetDevice(p_->device));
+  p_->enqueue_steps(nsteps);
+  LD_CK(cudaStreamSynchronize(p_->stream));
+  LD_CK(cudaGetLastError());
+}
+
+std::vector<double> Solver::l2_norm() {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  auto ss = s.reduce(s.samples.p, s.N, s.batch, s.N, nullptr, nullptr, 0, nullptr);
+  for (auto& x : ss) x = std::sqrt(x / (double)s.N);
+  return ss;
+}
+
+std::vector<double> Solver::energy() {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  std::vector<double> out(s.batch);
+  s.coef.alloc(s.N);
+  const double kin = 0.5 * s.eps * 4.0 * M_PI * M_PI;
+  for (long long m = 0; m < s.batch; ++m) {
+    const double2* sm = s.samples.p + m * s.N;
+    auto pot = s.reduce(sm, s.N, 1, s.N, s.v.p, nullptr, 0, nullptr);
+    s.analyze_dev(sm, s.coef.p, s.work.p);
+    auto kn = s.reduce(s.coef.p, s.N, 1, s.N, nullptr, s.nidx.p, kin, nullptr);
+    out[m] = kn[0] + pot[0] / (s.eps * (double)s.N);
+  }
+  return out;
+}
+
+double Solver::l2_distance(const std::complex<double>* ref, Space space, std::int64_t member) {
+  Impl& s = *p_;
+  if (member < 0 || member >= s.batch) raise(Errc::invalid_argument, "l2_distance: member out of range");
+  LD_CK(cudaSetDevice(s.device));
+  s.tmp.alloc(s.N);
+  LD_CK(cudaMemcpyAsync(s.tmp.p, ref, sizeof(double2) * s.N, cudaMemcpyHostToDevice, s.stream));
+  if (space == Space::coefficients) {
+    s.coef.alloc(s.N);
+    LD_CK(cudaMemcpyAsync(s.coef.p, s.tmp.p, sizeof(double2) * s.N, cudaMemcpyDeviceToDevice, s.stream));
+    s.synthesize_dev(s.coef.p, s.tmp.p, s.work.p);
+  }
+  auto d = s.reduce(s.samples.p + member * s.N, s.N, 1, s.N, nullptr, nullptr, 0, s.tmp.p);
+  return std::sqrt(d[0] / (double)s.N);
+}
+
+std::vector<TrajectoryRow> Solver::propagate(std::int64_t m, std::int64_t record_every, std::int64_t member) {
+  if (m < 0) raise(Errc::invalid_argument, "propagate: m must be >= 0");
+  if (record_every <= 0) record_every = m > 0 ? m : 1;
+  std::vector<TrajectoryRow> rows;
+  auto record = [&](std::int64_t k) {
+    rows.push_back({k, (double)k * p_->dt_, l2_norm()[member], energy()[member]});
+  };
+  record(0);
+  for (std::int64_t k = 0; k < m;) {
+    std::int64_t n = std::min(record_every, m - k);
+    step(n);
+    k += n;
+    record(k);
+  }
+  return rows;
+}
+
+double Solver::time_steps(std::int64_t nsteps) {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  cudaEvent_t a, b;
+  LD_CK(cudaEventCreate(&a));
+  LD_CK(cudaEventCreate(&b));
+  LD_CK(cudaEventRecord(a, s.stream));
+  s.enqueue_steps(nsteps);
+  LD_CK(cudaEventRecord(b, s.stream));
+  LD_CK(cudaEventSynchronize(b));
+  float ms = 0;
+  LD_CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  LD_CK(cudaGetLastError());
+  return ms;
+}
+
+void Solver::profile_passes(std::int64_t nsteps, double* ms_col, double* ms_row) {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  Impl::PassTimer pt;
+  s.enqueue_steps(nsteps, &pt);
+  LD_CK(cudaStreamSynchronize(s.stream));
+  auto avg = [](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+    double tot = 0;
+    for (auto& [a, b] : v) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      tot += ms;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+    return v.empty() ? 0.0 : tot / (double)v.size();
+  };
+  *ms_col = avg(pt.col);
+  *ms_row = avg(pt.row);
+}
+
+void Solver::flush_l2() {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  const size_t bytes = 512ull << 20;
+  if (!s.flush.p) s.flush.alloc(bytes);
+  LD_CK(cudaMemsetAsync(s.flush.p, (int)(s.launches & 0xff), bytes, s.stream));
+  LD_CK(cudaStreamSynchronize(s.stream));
+}
+
+void Solver::synchronize() {
+  LD_CK(cudaSetDevice(p_->device));
+  LD_CK(cudaStreamSynchronize(p_->stream));
+}
+
+SolverInfo Solver::info() const {
+  const Impl& s = *p_;
+  SolverInfo i{};
+  i.n_total = s.N;
+  i.batch = s.batch;
+  i.M = s.M;
+  i.M1 = s.M1;
+  i.M2 = s.M2;
+  i.rank = s.rank;
+  i.method = s.method;
+  i.group = s.group;
+  const double M = (double)s.M, N = (double)s.N, B = (double)s.batch;
+  if (s.rank == 2) {
+    i.bytes_per_pass_row = B * (32.0 * N + 16.0 * N);  // state R+W + V
+    i.bytes_per_pass_col = B * (32.0 * N + 2.0 * N);   // state R+W + D index
+    i.bytes_per_step = i.bytes_per_pass_row + i.bytes_per_pass_col;
+    i.launches_per_step = 2;
+  } else if (s.method == "circulant") {
+    const double G = (double)s.group, groups = std::ceil(B / G);
+    i.bytes_per_pass_col = B * (32.0 * M + 16.0 * N);  // state R+W + V (valid part)
+    i.bytes_per_pass_row = B * 32.0 * M + groups * 16.0 * M;  // state R+W + K^ once per group
+    i.bytes_per_step = i.bytes_per_pass_col + i.bytes_per_pass_row;
+    i.launches_per_step = 2 * (int)groups;
+  } else {
+    const double G = (double)s.group, groups = std::ceil(B / G);
+    i.bytes_per_pass_col = B * (32.0 * M + 9.0 * N);   // avg of (V 16N) and (D idx 2N)
+    i.bytes_per_pass_row = B * 32.0 * M + groups * 16.0 * M;
+    i.bytes_per_step = 2.0 * (i.bytes_per_pass_col + i.bytes_per_pass_row);
+    i.launches_per_step = 4 * (int)groups;
+  }
+  return i;
+}
+
+std::int64_t Solver::kernel_launches() const { return p_->launches; }
+
+}  // namespace lattdse

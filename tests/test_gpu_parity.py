@@ -1,0 +1,202 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the CPU oracle.
+
+Tolerances (BASELINE.json north_star): relative L2 difference of the wave
+function <= 1e-12 after one step and <= 1e-10 after the full run;
+| ||u|| - 1 | <= 1e-12 (norm conservation). Index maps / generating vectors are
+compared bit-exactly in the CPU tests.
+"""
+import numpy as np
+import pytest
+
+import paper_1808_06357_b200 as L
+from paper_1808_06357_b200 import configs
+from oracle.pyoracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL_ONE = 1e-12
+TOL_RUN = 1e-10
+TOL_NORM = 1e-12
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def make(lat, a, b, c, p, sigma, eps, dt, method="circulant", batch=None):
+    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    gen, moduli = lat.generators()
+    orc = Oracle(gen, moduli, norm2, eps, a, b)
+    orc.set_dt(dt)
+    S = L.Solver(lat, eps, a, b, c if batch is None else c[:batch], p if batch is None else p[:batch], sigma,
+                 method=method, norm2=norm2)
+    S.set_dt(dt)
+    S.discretize_initial()
+    return S, orc
+
+
+def oracle_coeffs(orc, c, p, sigma, steps):
+    g = orc.initial_samples(c, p, sigma)
+    u0 = orc.analyze(g)
+    return g, u0, orc.steps(u0, steps)
+
+
+@pytest.mark.parametrize("method", ["circulant", "bluestein"])
+@pytest.mark.parametrize("n,d", [(5, 1), (8, 1), (55, 2), (101, 3), (4099, 2), (16411, 4)])
+def test_rank1_small(n, d, method):
+    lat, a, b, c, p = configs.small_rank1(d, n, seed=11 + n)
+    eps, dt, sigma = 0.1, 1.0 / 64, 0.12
+    S, orc = make(lat, a, b, c, p, sigma, eps, dt, method)
+    g, u0, u1 = oracle_coeffs(orc, c[0], p[0], sigma, 1)
+    # discretisation matches the oracle's samples and coefficients
+    assert rel(S.get_state(L.SAMPLES)[0], g) <= 1e-14
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u0) <= 1e-13
+    S.step(1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u1) <= TOL_ONE
+    u10 = orc.steps(u1, 9)
+    S.step(9)
+    got = S.get_state(L.COEFFICIENTS)[0]
+    assert rel(got, u10) <= TOL_RUN
+    assert abs(S.l2_norm()[0] - orc.l2_norm(u10)) <= TOL_NORM
+    assert abs(S.energy()[0] - orc.energy(u10)) <= 1e-10 * abs(orc.energy(u10))
+
+
+def test_config0_full_run():
+    cfg = configs.CONFIGS["C0"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    S, orc = make(lat, a, b, c, p, cfg.sigma, cfg.eps, cfg.dt)
+    g, u0, u1 = oracle_coeffs(orc, c[0], p[0], cfg.sigma, 1)
+    S.step(1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u1) <= TOL_ONE
+    um = orc.steps(u1, cfg.m - 1)
+    S.step(cfg.m - 1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], um) <= TOL_RUN
+    assert abs(S.l2_norm()[0] - 1.0) <= TOL_NORM
+
+
+def test_config0_bluestein_matches_circulant():
+    cfg = configs.CONFIGS["C0"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    S1, _ = make(lat, a, b, c, p, cfg.sigma, cfg.eps, cfg.dt, "circulant")
+    S2, _ = make(lat, a, b, c, p, cfg.sigma, cfg.eps, cfg.dt, "bluestein")
+    S1.step(cfg.m)
+    S2.step(cfg.m)
+    assert rel(S1.get_state()[0], S2.get_state()[0]) <= TOL_RUN
+
+
+@pytest.mark.parametrize("n1,n2,d", [(4, 4, 2), (16, 16, 3), (64, 32, 4), (256, 256, 4)])
+def test_rank2_grid_small(n1, n2, d):
+    gen = [[1] + [2 * j + 1 for j in range(1, d)], [0] + [2 * j - 1 for j in range(1, d)]]
+    lat = L.Lattice.create(d, 2, gen, [n1, n2])
+    a, b, c, p = L.problem_draw(99 + n1, d, 1, 0.4, 0.6, 2)
+    eps, dt, sigma = 0.05, 1.0 / 32, 0.15
+    S, orc = make(lat, a, b, c, p, sigma, eps, dt)
+    g, u0, u1 = oracle_coeffs(orc, c[0], p[0], sigma, 1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u0) <= 1e-13
+    S.step(1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u1) <= TOL_ONE
+    u8 = orc.steps(u1, 7)
+    S.step(7)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u8) <= TOL_RUN
+
+
+def test_batch_members_independent():
+    lat, a, b, c, p = configs.small_rank1(3, 1021, seed=5, batch=6, c_range=(0.3, 0.7), p_max=3)
+    eps, dt, sigma = 0.05, 1.0 / 128, 0.1
+    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    gen, moduli = lat.generators()
+    orc = Oracle(gen, moduli, norm2, eps, a, b)
+    orc.set_dt(dt)
+    # groups of 4 and of 1 must give identical (bit-for-bit) results
+    outs = []
+    for group in (4, 1):
+        S = L.Solver(lat, eps, a, b, c, p, sigma, group=group, norm2=norm2)
+        S.set_dt(dt)
+        S.discretize_initial()
+        S.step(3)
+        outs.append(S.get_state())
+    assert np.array_equal(outs[0], outs[1])
+    for m in range(6):
+        _, _, u3 = oracle_coeffs(orc, c[m], p[m], sigma, 3)
+        assert rel(orc.analyze(outs[0][m]), u3) <= TOL_ONE * 10
+
+
+def test_time_reversibility_and_norm():
+    lat, a, b, c, p = configs.small_rank1(4, 16411, seed=3)
+    eps, dt, sigma = 0.1, 1.0 / 50, 0.1
+    S, _ = make(lat, a, b, c, p, sigma, eps, dt)
+    u0 = S.get_state()[0]
+    S.step(50)
+    assert abs(S.l2_norm()[0] - 1.0) <= TOL_NORM
+    S.set_dt(-dt)
+    S.step(50)
+    assert rel(S.get_state()[0], u0) <= 1e-10
+
+
+def test_commuting_case_constant_potential():
+    # v == const (a = b = 0 gives v = 0): splitting exact, u(T) = exp(-i eps T 2pi^2 |h|^2) u0
+    lat, _, _, c, p = configs.small_rank1(2, 4099, seed=2)
+    a = np.zeros(2)
+    b = np.zeros(1)
+    eps, dt, sigma = 0.1, 0.5, 0.1
+    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    S = L.Solver(lat, eps, a, b, c, p, sigma, norm2=norm2)
+    S.set_dt(dt)
+    S.discretize_initial()
+    u0 = S.get_state(L.COEFFICIENTS)[0]
+    S.step(2)
+    exact = u0 * np.exp(-1j * eps * 1.0 * 2 * np.pi ** 2 * norm2.astype(np.float64))
+    assert rel(S.get_state(L.COEFFICIENTS)[0], exact) <= 1e-10
+
+
+def test_config1_first_steps():
+    cfg = configs.CONFIGS["C1"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    S, orc = make(lat, a, b, c, p, cfg.sigma, cfg.eps, cfg.dt)
+    g, u0, u1 = oracle_coeffs(orc, c[0], p[0], cfg.sigma, 1)
+    S.step(1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u1) <= TOL_ONE
+    u4 = orc.steps(u1, 3)
+    S.step(3)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u4) <= TOL_ONE * 4
+
+
+def test_config1_full_run_invariants():
+    cfg = configs.CONFIGS["C1"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    S, _ = make(lat, a, b, c, p, cfg.sigma, cfg.eps, cfg.dt)
+    e0 = S.energy()[0]
+    S.step(cfg.m)
+    assert abs(S.l2_norm()[0] - 1.0) <= TOL_NORM
+    e1 = S.energy()[0]
+    assert abs(e1 - e0) <= 1e-3 * abs(e0)  # Strang energy error O(dt^2), bounded
+
+
+def test_config2_first_step():
+    cfg = configs.CONFIGS["C2"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    S, orc = make(lat, a, b, c, p, cfg.sigma, cfg.eps, cfg.dt)
+    g, u0, u1 = oracle_coeffs(orc, c[0], p[0], cfg.sigma, 1)
+    S.step(1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u1) <= TOL_ONE
+    S.step(cfg.m - 1)
+    assert abs(S.l2_norm()[0] - 1.0) <= TOL_NORM
+
+
+def test_config3_members_vs_oracle():
+    cfg = configs.CONFIGS["C3"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    batch = 8
+    S, orc = make(lat, a, b, c, p, cfg.sigma, cfg.eps, cfg.dt, batch=batch)
+    S.step(2)
+    got = S.get_state(L.COEFFICIENTS)
+    for m in (0, 3, 7):
+        _, _, u2 = oracle_coeffs(orc, c[m], p[m], cfg.sigma, 2)
+        assert rel(got[m], u2) <= TOL_ONE * 2
+    assert np.all(np.abs(S.l2_norm() - 1.0) <= TOL_NORM)
