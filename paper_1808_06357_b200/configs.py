@@ -7,9 +7,16 @@ ensemble member m draws (c, p) from a stream seeded with
 SplitMix64(base ^ (m+1)).next(). v and z are shared by all members.
 
 Generating vectors: paper_1808_06357_b200/catalog.json holds the prime-n CBC
-vectors (recomputed and compared by tests/test_cbc.py); the rank-2 lattice
-of config 2 is Z = [(1,3,...,15), (0,1,3,...,13)], n = (4096, 4096)
-(SURVEY.md §7 step 1), validated by Lattice.create like any other.
+vectors (recomputed and compared by tests/test_cbc.py). The reference has no
+rank-r constructor, so config 2 uses a product rank-2
+lattice built from the 8-D CBC vector z for n = 4096 (SPEC's power-of-two
+CBC, odd candidates): Z = [(z1..z4, 0,0,0,0), (0,0,0,0, z5..z8)],
+n = (4096, 4096). It is canonical (validated by Lattice.create: n2 | n1,
+nonzero components odd, independent columns, 4096^2 distinct points) and its
+minimal anti-aliasing set has max ||h||^2 = 96. The survey's example
+Z = [(1,3,..,15), (0,1,3,..,13)] also validates, but its dual lattice has
+short vectors: max ||h||^2 is already 163 at n = 128, so a norm table at
+n = 4096 is out of reach.
 """
 from __future__ import annotations
 
@@ -64,8 +71,9 @@ def _c(name, index, d, n, eps, T, m, sigma, batch=1, c_range=(0.4, 0.6), p_max=2
 CONFIGS = {
     "C0": _c("C0", 0, 2, 4099, 0.1, 1.0, 256, 0.1),
     "C1": _c("C1", 1, 6, 1048583, 0.05, 1.0, 1024, 0.1),
+    # product rank-2 lattice from the 8-D CBC vector for n = 4096 (see module doc)
     "C2": _c("C2", 2, 8, None, 0.05, 1.0, 512, 0.08, rank=2, moduli=(4096, 4096),
-             gen=[[1, 3, 5, 7, 9, 11, 13, 15], [0, 1, 3, 5, 7, 9, 11, 13]]),
+             gen=[[1, 1557, 1741, 1031, 0, 0, 0, 0], [0, 0, 0, 0, 363, 1705, 1349, 1667]]),
     "C3": _c("C3", 3, 6, 262147, 0.05, 0.5, 512, 0.1, batch=512, c_range=(0.3, 0.7), p_max=3),
     "C4": _c("C4", 4, 20, 1073741827, 0.02, 0.1, 64, 0.15),
 }
@@ -98,3 +106,13 @@ def small_rank1(d: int, n: int, eps=0.1, sigma=0.1, seed=7, batch=1, c_range=(0.
     lat = Lattice.rank1(z, n)
     a, b, c, p = problem_draw(seed, d, batch, c_range[0], c_range[1], p_max)
     return lat, a, b, c, p
+
+
+def rank2_product(n1: int, n2: int, d: int):
+    """Product rank-2 lattice as used by config 2: CBC vector z for n1 in d
+    dimensions, Z = [(z_1..z_h, 0..0), (0..0, z_{h+1}..z_d) mod n2], h = d//2."""
+    z, _ = cbc_construct(n1, d)
+    h = d // 2
+    c1 = [int(x) for x in z[:h]] + [0] * (d - h)
+    c2 = [0] * h + [int(x) % n2 for x in z[h:]]
+    return Lattice.create(d, 2, [c1, c2], [n1, n2])

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <random>
 #include <vector>
+#include <string>
 
 #include "fft_pass.cuh"
 
@@ -259,7 +260,45 @@ template <int M1, int M2> void test_fourstep(long long nvalid) {
   check(buf, e / mx, 1e-14);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "c1") {
+    const long long M1 = 1215, M2 = 1728, M = M1 * M2;
+    const long long N = 1048583;
+    std::vector<double2> buf(M, make_double2(1.0, 0.5)), inN(N, make_double2(0.5, 0.25)), dN(N, make_double2(1, 0));
+    Tables t1;
+    t1.build(M1, M);
+    PassArgs a{};
+    a.in = inN.data();
+    a.out = buf.data();
+    a.in_bstride = N;
+    a.out_bstride = M;
+    a.nvalid_in = N;
+    a.nvalid_mid = a.nvalid_out = M;
+    a.ncols = M2;
+    a.nlines = M2;
+    a.post_tw = 1;
+    a.diag_kind = DG_CPLX;
+    a.diag = dN.data();
+    a.fft_tw = t1.fft_tw.data();
+    a.tw_lo = t1.tw_lo.data();
+    a.tw_hi = t1.tw_hi.data();
+    a.tw_shift = t1.shift;
+    std::printf("tw_lo %zu tw_hi %zu shift %d\n", t1.tw_lo.size(), t1.tw_hi.size(), t1.shift);
+    emulate<AX_COL, 1215, 2, 256, PROG_LOADDIAG, -1>(a, M2, 1);
+    std::printf("c1 col entry emulated ok %f\n", buf[12345].x);
+    return 0;
+  }
+  if (argc > 1) {
+    test_lines<AX_COL, 1215, 2, 256, -1>(4);
+    test_lines<AX_COL, 1215, 2, 256, 1>(3);
+    test_double<AX_COL, 1215, 2, 256, 1>(4, 1000);
+    test_lines<AX_ROW, 1728, 1, 224, -1>(2);
+    test_double<AX_ROW, 1728, 1, 224, -1>(2, 100000);
+    test_lines<AX_COL, 4096, 2, 256, -1>(2);
+    test_double<AX_ROW, 4096, 1, 256, 1>(1, 100000);
+    return g_fail;
+  }
+
   test_dft<2, -1>(); test_dft<3, -1>(); test_dft<4, -1>(); test_dft<5, -1>();
   test_dft<6, -1>(); test_dft<8, -1>(); test_dft<9, -1>(); test_dft<10, -1>();
   test_dft<12, -1>(); test_dft<15, -1>(); test_dft<16, -1>(); test_dft<18, 1>();

@@ -84,8 +84,10 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
     long long j = nat(b, i);
     double2 v = make_double2(0.0, 0.0);
     if (!live(b)) return v;
-    if (j < a->nvalid_in) v = a->in[bat * a->in_bstride + j];
-    if (PROG == PROG_LOADDIAG) v = apply_diag(v, j);
+    if (j < a->nvalid_in) {
+      v = a->in[bat * a->in_bstride + j];
+      if (PROG == PROG_LOADDIAG) v = apply_diag(v, j);  // diag tables hold nvalid_in entries
+    }
     if (AXIS == AX_COL && a->pre_tw) v = c_mulc(v, twid(tw_index(b, i)));
     return v;
   }
@@ -93,8 +95,9 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
     if (!live(b)) return;
     if (AXIS == AX_COL && a->post_tw) v = c_mul(v, twid(tw_index(b, i)));
     long long j = nat(b, i);
+    if (j >= a->nvalid_out) return;
     if (PROG == PROG_STOREDIAG) v = apply_diag(v, j);
-    if (j < a->nvalid_out) a->out[bat * a->out_bstride + j] = v;
+    a->out[bat * a->out_bstride + j] = v;
   }
   LD_HD double2 mid(int b, int i, double2 v) const {
     long long j = nat(b, i);

@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -220,6 +222,7 @@ struct Solver::Impl {
   DBuf<char> flush;
   bool bluestein_tables = false;
   long long launches = 0;
+  bool sync_check = std::getenv("LATTDSE_SYNC_CHECK") != nullptr;  // debug: sync after every launch
 
   explicit Impl(const Lattice& l) : lat(l) {}
 
@@ -236,11 +239,33 @@ struct Solver::Impl {
     void* args[] = {&a};
     LD_CK(cudaLaunchKernel(k->fn, grid, dim3(k->NT), args, (size_t)k->smem, stream));
     ++launches;
+    if (sync_check) {
+      cudaError_t e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) {
+        std::fprintf(stderr,
+                     "pass fault: in=%p out=%p bstr=%lld/%lld nvalid=%lld/%lld/%lld ncols=%d nlines=%d dk=%d diag=%p "
+                     "idx=%p lut=%p tw=%d/%d/%d lo=%p hi=%p fft_tw=%p | work=%p(%zu) M=%lld M1=%lld M2=%lld N=%lld "
+                     "twcol=%p(%zu) twrow=%p(%zu) lo=%p(%zu) hi=%p(%zu) B1=%p B2=%p K=%p\n",
+                     (const void*)a.in, (void*)a.out, a.in_bstride, a.out_bstride, a.nvalid_in, a.nvalid_mid,
+                     a.nvalid_out, a.ncols, a.nlines, a.diag_kind, (const void*)a.diag, a.diag_idx, (const void*)a.lut,
+                     a.pre_tw, a.post_tw, a.tw_shift, (const void*)a.tw_lo, (const void*)a.tw_hi,
+                     (const void*)a.fft_tw, (void*)work.p, work.n, M, M1, M2, N, (void*)tw_col.p, tw_col.n,
+                     (void*)tw_row.p, tw_row.n, (void*)tw_lo.p, tw_lo.n, (void*)tw_hi.p, tw_hi.n, (void*)B1hat.p,
+                     (void*)B2hat.p, (void*)Khat.p);
+        raise(Errc::device_error, "pass axis=" + std::to_string(axis) + " L=" + std::to_string(L) + " prog=" +
+                                      std::to_string(prog) + " sign=" + std::to_string(sign) + " grid=" +
+                                      std::to_string(grid.x) + "x" + std::to_string(grid.y) + ": " + cudaGetErrorString(e));
+      }
+    }
   }
   int grid1d(long long n) const { return (int)std::min<long long>((n + 255) / 256, 148 * 16); }
-  void aux_done() {
+  void aux_done(const char* what = "aux") {
     LD_CK(cudaGetLastError());
     ++launches;
+    if (sync_check) {
+      cudaError_t e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) raise(Errc::device_error, std::string(what) + ": " + cudaGetErrorString(e));
+    }
   }
 
   PassArgs base_args(int axis) const {
@@ -400,15 +425,15 @@ struct Solver::Impl {
     chirp_c.alloc(N);
     chirp_n.alloc(N);
     k_chirp<<<grid1d(N), 256, 0, stream>>>(N, chirp.p, chirp_c.p, chirp_n.p);
-    aux_done();
+    aux_done("k_chirp");
     // B1 = FFT_M(wrap conj c)/M (forward DFT), B2 = FFT_M(wrap c)/M (inverse)
     B1hat.alloc(M);
     B2hat.alloc(M);
     k_wrap<<<grid1d(M), 256, 0, stream>>>(chirp_c.p, N, M, 1.0 / (double)M, 1, B1hat.p);
-    aux_done();
+    aux_done("k_wrap");
     r1_fft_table_full(B1hat.p);
     k_wrap<<<grid1d(M), 256, 0, stream>>>(chirp.p, N, M, 1.0 / (double)M, 1, B2hat.p);
-    aux_done();
+    aux_done("k_wrap");
     r1_fft_table_full(B2hat.p);
     bluestein_tables = true;
   }
@@ -452,9 +477,9 @@ struct Solver::Impl {
     V.alloc(N);
     Vh.alloc(N);
     k_phase<<<grid1d(N), 256, 0, stream>>>(v.p, N, -dt / eps, V.p);
-    aux_done();
+    aux_done("k_phase");
     k_phase<<<grid1d(N), 256, 0, stream>>>(v.p, N, -dt / (2.0 * eps), Vh.p);
-    aux_done();
+    aux_done("k_phase");
     // kinetic LUT exp(-i eps dt 2 pi^2 s)/N for s = 0..max ||h||^2
     std::vector<double2> lut(max_norm2 + 1);
     for (std::uint32_t s = 0; s <= max_norm2; ++s) {
@@ -473,14 +498,14 @@ struct Solver::Impl {
         // wrap periodically into length M, K^ = FFT_M(K)/M.
         kin_full.alloc(N);
         k_lut_gather<<<grid1d(N), 256, 0, stream>>>(nidx.p, kin_lut.p, N, kin_full.p);
-        aux_done();
+        aux_done("k_lut_gather");
         tmp.alloc(std::max<long long>(N, 1));
         DBuf<double2> scratch;
         scratch.alloc(M);
         synthesize_dev(kin_full.p, tmp.p, scratch.p);
         Khat.alloc(M);
         k_wrap<<<grid1d(M), 256, 0, stream>>>(tmp.p, N, M, 1.0 / (double)M, 0, Khat.p);
-        aux_done();
+        aux_done("k_wrap");
         r1_fft_table_full(Khat.p);
         LD_CK(cudaStreamSynchronize(stream));
         kin_full.release();
@@ -490,9 +515,9 @@ struct Solver::Impl {
         Ventry.alloc(N);
         Vexit.alloc(N);
         k_mul<<<grid1d(N), 256, 0, stream>>>(Vh.p, chirp.p, N, Ventry.p);
-        aux_done();
+        aux_done("k_mul");
         k_mul<<<grid1d(N), 256, 0, stream>>>(Vh.p, chirp_c.p, N, Vexit.p);
-        aux_done();
+        aux_done("k_mul");
       }
     }
     LD_CK(cudaStreamSynchronize(stream));
@@ -563,7 +588,7 @@ struct Solver::Impl {
     const int blocks = (int)std::min<long long>((n + 255) / 256, 592);
     partial.alloc((size_t)blocks * nb);
     k_wsumsq<<<dim3(blocks, (unsigned)nb), 256, 0, stream>>>(x, n, bstride, w, widx, wscale, y, partial.p);
-    aux_done();
+    aux_done("k_wsumsq");
     std::vector<double> h((size_t)blocks * nb);
     LD_CK(cudaMemcpyAsync(h.data(), partial.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
     LD_CK(cudaStreamSynchronize(stream));

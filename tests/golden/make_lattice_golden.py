@@ -98,8 +98,12 @@ def main():
     cases.append(case(lib, 4, 2, [[1, 3, 5, 7], [0, 1, 3, 5]], [8, 4], [[1, 2, 3, 4], [-2, 0, 1, 9]]))
     cases.append(case(lib, 3, 1, [[1, 0, 7]], [16], [[1, 1, 1], [0, 3, -2]]))   # zero component allowed
     cases.append(case(lib, 3, 2, [[2, 0, 0], [0, 1, 0]], [4, 4]))         # non_coprime (2 vs 4)
-    # the BASELINE rank-2 lattice of config 2
+    # the survey's example rank-2 generator (validates; not used: poor aaset)
     z2 = [[1, 3, 5, 7, 9, 11, 13, 15], [0, 1, 3, 5, 7, 9, 11, 13]]
+    hs = rng.integers(-9, 10, size=(16, 8)).tolist()
+    cases.append(case(lib, 8, 2, z2, [4096, 4096], hs, point_rows=[0, 1, 4095, 4096, 4097, 16777215]))
+    # the rank-2 lattice of config 2 (product of the 8-D CBC vector halves)
+    z2 = [[1, 1557, 1741, 1031, 0, 0, 0, 0], [0, 0, 0, 0, 363, 1705, 1349, 1667]]
     hs = rng.integers(-9, 10, size=(16, 8)).tolist()
     cases.append(case(lib, 8, 2, z2, [4096, 4096], hs, point_rows=[0, 1, 4095, 4096, 4097, 16777215]))
     # the rank-1 config lattices with our CBC vectors

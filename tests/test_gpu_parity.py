@@ -88,8 +88,7 @@ def test_config0_bluestein_matches_circulant():
 
 @pytest.mark.parametrize("n1,n2,d", [(4, 4, 2), (16, 16, 3), (64, 32, 4), (256, 256, 4)])
 def test_rank2_grid_small(n1, n2, d):
-    gen = [[1] + [2 * j + 1 for j in range(1, d)], [0] + [2 * j - 1 for j in range(1, d)]]
-    lat = L.Lattice.create(d, 2, gen, [n1, n2])
+    lat = configs.rank2_product(n1, n2, d)
     a, b, c, p = L.problem_draw(99 + n1, d, 1, 0.4, 0.6, 2)
     eps, dt, sigma = 0.05, 1.0 / 32, 0.15
     S, orc = make(lat, a, b, c, p, sigma, eps, dt)
