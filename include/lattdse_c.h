@@ -140,6 +140,8 @@ int lattdse_solver_time_steps(lattdse_solver* s, int64_t nsteps, double* ms);
 int lattdse_solver_profile_passes(lattdse_solver* s, int64_t nsteps, double* ms_col, double* ms_row);
 int lattdse_solver_flush_l2(lattdse_solver* s);
 int lattdse_solver_kernel_launches(lattdse_solver* s, int64_t* out);
+/* wait for all work queued on the solver stream */
+int lattdse_solver_synchronize(lattdse_solver* s);
 
 #ifdef __cplusplus
 }

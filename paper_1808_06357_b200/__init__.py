@@ -348,6 +348,9 @@ class Solver:
         _ck(_lib.lattdse_solver_profile_passes(self._h, C.c_int64(nsteps), C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def synchronize(self):
+        _ck(_lib.lattdse_solver_synchronize(self._h))
+
     def flush_l2(self):
         _ck(_lib.lattdse_solver_flush_l2(self._h))
 

@@ -460,4 +460,11 @@ int lattdse_solver_kernel_launches(lattdse_solver* s, int64_t* out) {
   });
 }
 
+int lattdse_solver_synchronize(lattdse_solver* s) {
+  return guard([&] {
+    LD_NEED_S();
+    s->s->synchronize();
+  });
+}
+
 }  // extern "C"
