@@ -131,6 +131,38 @@ template <int SIGN> struct DFT<5, SIGN> {
   }
 };
 
+// Odd prime P via the symmetric pairs (x_m +- x_{P-m}); used for P = 7.
+template <int P, int SIGN> struct DFT_ODDPRIME {
+  LD_HD static void run(double2* x) {
+    constexpr int H = (P - 1) / 2;
+    double2 sp[H], sm[H];
+    sfor<H>([&](auto mc) {
+      constexpr int m = decltype(mc)::value + 1;
+      sp[m - 1] = c_add(x[m], x[P - m]);
+      sm[m - 1] = c_sub(x[m], x[P - m]);
+    });
+    const double2 x0 = x[0];
+    double2 y0 = x0;
+    sfor<H>([&](auto mc) { y0 = c_add(y0, sp[decltype(mc)::value]); });
+    sfor<H>([&](auto kc) {
+      constexpr int k = decltype(kc)::value + 1;
+      double2 a = x0, b = make_double2(0.0, 0.0);
+      sfor<H>([&](auto mc) {
+        constexpr int m = decltype(mc)::value + 1;
+        constexpr int km = (k * m) % P;
+        constexpr double c = TwC<P, km>::c, sn = TwC<P, km>::s;
+        a = make_double2(fma(c, sp[m - 1].x, a.x), fma(c, sp[m - 1].y, a.y));
+        b = make_double2(fma(sn, sm[m - 1].x, b.x), fma(sn, sm[m - 1].y, b.y));
+      });
+      const double2 ib = c_muli<SIGN>(b);
+      x[k] = c_add(a, ib);
+      x[P - k] = c_sub(a, ib);
+    });
+    x[0] = y0;
+  }
+};
+template <int SIGN> struct DFT<7, SIGN> : DFT_ODDPRIME<7, SIGN> {};
+
 // Cooley-Tukey R = R1*R2 with constant inner twiddles.
 // input n = R2*n1 + n2, output k = k1 + R1*k2.
 template <int R1, int R2, int SIGN> struct DFT_CT {
@@ -203,39 +235,71 @@ template <int SIGN> struct DFT<18, SIGN> : DFT_PFA<2, 9, SIGN> {};
 template <int SIGN> struct DFT<20, SIGN> : DFT_PFA<4, 5, SIGN> {};
 template <int SIGN> struct DFT<24, SIGN> : DFT_PFA<3, 8, SIGN> {};
 template <int SIGN> struct DFT<27, SIGN> : DFT_CT<3, 9, SIGN> {};
+template <int SIGN> struct DFT<14, SIGN> : DFT_PFA<2, 7, SIGN> {};
+template <int SIGN> struct DFT<21, SIGN> : DFT_PFA<3, 7, SIGN> {};
+template <int SIGN> struct DFT<28, SIGN> : DFT_PFA<4, 7, SIGN> {};
 template <int SIGN> struct DFT<32, SIGN> : DFT_CT<4, 8, SIGN> {};
 
 // ------------------------------------------------------------ radix plan
-// Greedy factorisation of a transform length into in-register radices.
-constexpr int kRadixPref[] = {16, 15, 12, 9, 10, 8, 6, 5, 4, 3, 2};
+// Factorisation of a transform length into in-register radices. Stage 0 takes
+// the largest odd radix >= 9 when there is one, so its stride-R shared-memory
+// writes are bank-conflict free; otherwise (power-of-two-ish lengths) the
+// shared-memory layout is swizzled instead (Plan::swizzle).
+constexpr int kRadixPref[] = {16, 15, 12, 14, 9, 10, 8, 7, 6, 5, 4, 3, 2};
 
 constexpr int pick_radix(int rem) {
   for (int r : kRadixPref)
     if (rem % r == 0) return r;
   return rem;  // rejected by the static_assert in Plan
 }
+constexpr int first_radix(int L) {
+  for (int r : {21, 15, 9})
+    if (L % r == 0) return r;
+  return pick_radix(L);
+}
 
 template <int L> struct Plan {
+  static constexpr int radix(int s) {
+    int rem = L;
+    int r = first_radix(L);
+    for (int i = 0; i < s; ++i) {
+      rem /= r;
+      r = pick_radix(rem);
+    }
+    return r;
+  }
   static constexpr int count() {
     int n = 0, rem = L;
     while (rem > 1) {
-      rem /= pick_radix(rem);
+      rem /= radix(n);
       ++n;
     }
     return n;
   }
   static constexpr int nst = count();
-  static constexpr int radix(int s) {
-    int rem = L;
-    for (int i = 0; i < s; ++i) rem /= pick_radix(rem);
-    return pick_radix(rem);
-  }
   // Ns = product of the radices of the earlier stages
   static constexpr int ns(int s) {
     int p = 1;
     for (int i = 0; i < s; ++i) p *= radix(i);
     return p;
   }
+  static constexpr int max_tasks() {
+    int m = 0;
+    for (int s = 0; s < nst; ++s) m = (L / radix(s)) > m ? (L / radix(s)) : m;
+    return m;
+  }
+  // Per-stage twiddle table: stage s >= 1 owns (R_s - 1) * Ns_s entries
+  // laid out [r-1][k] = exp(-2 pi i r k / (Ns_s R_s)), so the threads of a
+  // warp (consecutive k) read consecutive entries.
+  static constexpr int tw_offset(int s) {
+    int o = 0;
+    for (int i = 1; i < s; ++i) o += (radix(i) - 1) * ns(i);
+    return o;
+  }
+  static constexpr int tw_size = tw_offset(nst);
+  // even first radix -> stride-R stage-0 writes conflict; pad 1 slot per 16
+  static constexpr bool swizzle = (radix(0) % 2 == 0) && L >= 16;
+  static constexpr int phys(int i) { return swizzle ? i + (i >> 4) : i; }
   static constexpr bool valid() {
     for (int s = 0; s < nst; ++s) {
       int r = radix(s);
@@ -245,5 +309,31 @@ template <int L> struct Plan {
   }
   static_assert(valid(), "transform length must factor into radices <= 32 from kRadixPref");
 };
+
+// Host: per-stage twiddle table for a radix plan (layout of Plan::tw_offset),
+// correctly rounded via long double. out must hold sum_{s>=1} (R_s-1) Ns_s.
+inline int build_stage_twiddles(const int* radix, int nst, double2* out) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  int o = 0, ns = radix[0];
+  for (int s = 1; s < nst; ++s) {
+    const int R = radix[s];
+    const long long len = (long long)ns * R;
+    for (int r = 1; r < R; ++r)
+      for (int k = 0; k < ns; ++k) {
+        const long long q = ((long long)r * k) % len;
+        const long double a = -2.0L * pi * (long double)q / (long double)len;
+        if (out) out[o] = make_double2((double)cosl(a), (double)sinl(a));
+        ++o;
+      }
+    ns *= R;
+  }
+  return o;
+}
+
+template <int L> inline int plan_twiddles(double2* out) {
+  int radix[32];
+  for (int s = 0; s < Plan<L>::nst; ++s) radix[s] = Plan<L>::radix(s);
+  return build_stage_twiddles(radix, Plan<L>::nst, out);
+}
 
 }  // namespace lattdse_dev

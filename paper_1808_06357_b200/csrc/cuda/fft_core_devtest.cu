@@ -36,8 +36,8 @@ int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin
   for (auto& v : x) v = make_double2(u(rng), u(rng));
   for (auto& v : diag) v = make_double2(u(rng), u(rng));
   for (auto& v : xin) v = make_double2(u(rng), u(rng));
-  std::vector<double2> fft_tw(L);
-  for (int t = 0; t < L; ++t) fft_tw[t] = root(t, L);
+  std::vector<double2> fft_tw(std::max(1, plan_twiddles<L>(nullptr)));
+  plan_twiddles<L>(fft_tw.data());
   int shift = 0;
   while ((1LL << (2 * shift)) < M) ++shift;
   long long nlo = 1LL << shift, nhi = (M + nlo - 1) / nlo;
@@ -46,11 +46,11 @@ int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin
   for (long long t = 0; t < nhi; ++t) hi[t] = root(t * nlo, M);
   double2 *dx, *dd, *dtw, *dlo, *dhi, *din;
   CK(cudaMalloc(&dx, M * 16)); CK(cudaMalloc(&dd, NI * 16)); CK(cudaMalloc(&din, NI * 16));
-  CK(cudaMemcpy(din, xin.data(), NI * 16, cudaMemcpyHostToDevice)); CK(cudaMalloc(&dtw, L * 16));
+  CK(cudaMemcpy(din, xin.data(), NI * 16, cudaMemcpyHostToDevice)); CK(cudaMalloc(&dtw, fft_tw.size() * 16));
   CK(cudaMalloc(&dlo, nlo * 16)); CK(cudaMalloc(&dhi, nhi * 16));
   CK(cudaMemcpy(dx, x.data(), M * 16, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dd, diag.data(), NI * 16, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(dtw, fft_tw.data(), L * 16, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dtw, fft_tw.data(), fft_tw.size() * 16, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dlo, lo.data(), nlo * 16, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dhi, hi.data(), nhi * 16, cudaMemcpyHostToDevice));
   PassArgs a{};
@@ -75,7 +75,7 @@ int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin
   h.in = nin > 0 ? xin.data() : hx.data(); h.out = hx.data(); h.diag = diag.data(); h.fft_tw = fft_tw.data(); h.tw_lo = lo.data(); h.tw_hi = hi.data();
   std::vector<double2> sm(SmemGeom<L, B>::LS * B);
   for (long long blk = 0; blk < (nlines + B - 1) / B; ++blk) {
-    Ctx<AXIS, L, B, PROG> c{sm.data(), &h, (int)(blk * B), 0};
+    Ctx<AXIS, L, B, PROG> c{sm.data(), h, (int)(blk * B), 0};
     run_pass<HostExec, AXIS, L, B, NT, PROG, SIGN>(c);
   }
   double e = 0, mx = 0;

@@ -75,9 +75,11 @@ struct Tables {
   std::vector<double2> fft_tw;
   std::vector<double2> tw_lo, tw_hi;
   int shift = 0;
+  template <int L> void build_plan() {
+    fft_tw.resize(std::max(1, plan_twiddles<L>(nullptr)));
+    plan_twiddles<L>(fft_tw.data());
+  }
   void build(int L, long long M) {
-    fft_tw.resize(L);
-    for (int t = 0; t < L; ++t) fft_tw[t] = root(t, L, -1);
     shift = 0;
     while ((1LL << (2 * shift)) < M) ++shift;
     long long nlo = 1LL << shift, nhi = (M + nlo - 1) / nlo;
@@ -93,9 +95,91 @@ void emulate(PassArgs a, int nlines, int nbatch) {
   std::vector<double2> sm(SmemGeom<L, B>::LS * B);
   for (int bat = 0; bat < nbatch; ++bat)
     for (int blk = 0; blk < (nlines + B - 1) / B; ++blk) {
-      Ctx<AXIS, L, B, PROG> c{sm.data(), &a, blk * B, bat};
+      Ctx<AXIS, L, B, PROG> c{sm.data(), a, blk * B, bat};
       run_pass<HostExec, AXIS, L, B, NT, PROG, SIGN1>(c);
     }
+}
+
+// v2 path: host copy of load_tile (zero-fill semantics) + SRC_TILE stages.
+template <int AXIS, int L, int B, int NT, int SIGN1>
+void emulate_v2(PassArgs a, int nlines, int nbatch) {
+  using C = Ctx<AXIS, L, B, PROG_DOUBLE>;
+  std::vector<double2> sm(SmemGeom<L, B>::LS * B), dg(B * L);
+  const int nblk = (nlines + B - 1) / B;
+  for (int t = 0; t < nblk * nbatch; ++t) {
+    const int line0 = (t % nblk) * B;
+    const long long bat = t / nblk;
+    for (int q = 0; q < B * L; ++q) {
+      int b, i;
+      TileWalk<AXIS, L, B>::elem(q, b, i);
+      const bool live = line0 + b < a.nlines;
+      const long long j = AXIS == AX_ROW ? (long long)(line0 + b) * L + i : (long long)i * a.ncols + (line0 + b);
+      sm[C::slot(b, i)] = (live && j < a.nvalid_in) ? a.in[bat * a.in_bstride + j] : make_double2(0, 0);
+      dg[b * L + i] = (live && j < a.nvalid_mid) ? a.diag[j] : make_double2(0, 0);
+    }
+    C c{sm.data(), a, line0, bat, dg.data()};
+    run_pass<HostExec, AXIS, L, B, NT, PROG_DOUBLE, SIGN1, SRC_TILE>(c);
+  }
+}
+
+// v2 double program with a complex diag vs naive DFTs
+template <int AXIS, int L, int B, int NT, int SIGN1> void test_double_v2(int other, long long nmid, int pre, int post) {
+  int nrows = AXIS == AX_ROW ? other : L, ncols = AXIS == AX_ROW ? L : other;
+  std::mt19937_64 rng(L * 29 + AXIS + 3);
+  std::uniform_real_distribution<double> u(-1, 1);
+  long long n = (long long)nrows * ncols;
+  std::vector<double2> x(n), y(n), diag(n);
+  for (auto& v : x) v = make_double2(u(rng), u(rng));
+  for (auto& v : diag) v = make_double2(u(rng), u(rng));
+  y = x;
+  Tables tb;
+  tb.build(L, n);
+  tb.template build_plan<L>();
+  PassArgs a{};
+  a.in = y.data();
+  a.out = y.data();
+  a.in_bstride = a.out_bstride = n;
+  a.nvalid_in = a.nvalid_out = n;
+  a.nvalid_mid = nmid;
+  a.ncols = ncols;
+  a.nlines = AXIS == AX_ROW ? nrows : ncols;
+  a.diag_kind = DG_CPLX;
+  a.diag = diag.data();
+  a.pre_tw = pre;
+  a.post_tw = post;
+  a.fft_tw = tb.fft_tw.data();
+  a.tw_lo = tb.tw_lo.data();
+  a.tw_hi = tb.tw_hi.data();
+  a.tw_shift = tb.shift;
+  emulate_v2<AXIS, L, B, NT, SIGN1>(a, AXIS == AX_ROW ? nrows : ncols, 1);
+  auto tw = [&](long long t) {
+    long double ang = -2.0L * kPi * (long double)(t % n) / (long double)n;
+    return cld(cosl(ang), sinl(ang));
+  };
+  double e = 0, mx = 0;
+  for (int line = 0; line < (AXIS == AX_ROW ? nrows : ncols); ++line) {
+    std::vector<cld> v(L);
+    auto idx = [&](int i) { return AXIS == AX_ROW ? (long long)line * L + i : (long long)i * ncols + line; };
+    for (int i = 0; i < L; ++i) {
+      v[i] = cld(x[idx(i)].x, x[idx(i)].y);
+      if (AXIS == AX_COL && pre) v[i] *= std::conj(tw((long long)line * i));
+    }
+    auto w = naive_dft(v, SIGN1);
+    for (int i = 0; i < L; ++i) {
+      long long j = idx(i);
+      w[i] = j < nmid ? w[i] * cld(diag[j].x, diag[j].y) : cld(0);
+    }
+    auto z = naive_dft(w, -SIGN1);
+    for (int i = 0; i < L; ++i) {
+      if (AXIS == AX_COL && post) z[i] *= tw((long long)line * i);
+      long long j = idx(i);
+      e = std::max(e, (double)std::abs(z[i] - cld(y[j].x, y[j].y)));
+      mx = std::max(mx, (double)std::abs(z[i]));
+    }
+  }
+  char buf[96];
+  std::snprintf(buf, sizeof buf, "v2 double axis=%d L=%d B=%d NT=%d sign=%+d", AXIS, L, B, NT, SIGN1);
+  check(buf, e / mx, 4e-16 * 60);
 }
 
 // Lines along the contiguous (ROW) or strided (COL) axis: single transform.
@@ -114,6 +198,7 @@ template <int AXIS, int L, int B, int NT, int SIGN> void test_lines(int other) {
   }
   Tables tb;
   tb.build(L, 4);
+  tb.template build_plan<L>();
   PassArgs a{};
   a.in = x.data();
   a.out = y.data();
@@ -167,6 +252,7 @@ template <int AXIS, int L, int B, int NT, int SIGN1> void test_double(int other,
   y = x;
   Tables tb;
   tb.build(L, 4);
+  tb.template build_plan<L>();
   PassArgs a{};
   a.in = y.data();
   a.out = y.data();
@@ -217,6 +303,8 @@ template <int M1, int M2> void test_fourstep(long long nvalid) {
   Tables t1, t2;
   t1.build(M1, M);
   t2.build(M2, M);
+  t1.template build_plan<M1>();
+  t2.template build_plan<M2>();
   PassArgs a{};
   a.in = x.data();
   a.out = work.data();
@@ -260,6 +348,75 @@ template <int M1, int M2> void test_fourstep(long long nvalid) {
   check(buf, e / mx, 1e-14);
 }
 
+// Good-Thomas forward DFT of length M = M1*M2 (gcd 1): COL(LOADDIAG, pfa
+// gather from natural order) then ROW(FFT). X[k] lands at (k mod M1, k mod M2).
+template <int M1, int M2> void test_pfa(long long nvalid) {
+  const long long M = (long long)M1 * M2;
+  std::mt19937_64 rng(M + 5);
+  std::uniform_real_distribution<double> u(-1, 1);
+  std::vector<double2> x(nvalid), work(M), dg(nvalid);
+  for (auto& v : x) v = make_double2(u(rng), u(rng));
+  for (auto& v : dg) v = make_double2(u(rng), u(rng));
+  Tables t1, t2;
+  t1.template build_plan<M1>();
+  t2.template build_plan<M2>();
+  PassArgs a{};
+  a.in = x.data();
+  a.out = work.data();
+  a.in_bstride = nvalid;
+  a.out_bstride = M;
+  a.nvalid_in = nvalid;
+  a.nvalid_mid = a.nvalid_out = M;
+  a.ncols = M2;
+  a.nlines = M2;
+  a.diag_kind = DG_CPLX;
+  a.diag = dg.data();
+  a.fft_tw = t1.fft_tw.data();
+  a.pfa = 1;
+  a.pM1 = M1;
+  a.pM2 = M2;
+  a.pM = M;
+  emulate<AX_COL, M1, 2, 64, PROG_LOADDIAG, -1>(a, M2, 1);
+  PassArgs b{};
+  b.in = work.data();
+  b.out = work.data();
+  b.in_bstride = b.out_bstride = M;
+  b.nvalid_in = b.nvalid_mid = b.nvalid_out = M;
+  b.ncols = M2;
+  b.nlines = M1;
+  b.fft_tw = t2.fft_tw.data();
+  emulate<AX_ROW, M2, 1, 64, PROG_LOADDIAG, -1>(b, M1, 1);
+  std::vector<cld> xv(M, cld(0));
+  for (long long j = 0; j < nvalid; ++j) xv[j] = cld(x[j].x, x[j].y) * cld(dg[j].x, dg[j].y);
+  auto X = naive_dft(xv, -1);
+  double e = 0, mx = 0;
+  for (long long k = 0; k < M; ++k) {
+    long long p = (k % M1) * M2 + (k % M2);
+    e = std::max(e, (double)std::abs(cld(work[p].x, work[p].y) - X[k]));
+    mx = std::max(mx, (double)std::abs(X[k]));
+  }
+  // inverse: ROW IFFT then COL STOREDIAG (pfa scatter to natural order, x diag)
+  PassArgs c = b;
+  emulate<AX_ROW, M2, 1, 64, PROG_LOADDIAG, 1>(c, M1, 1);
+  std::vector<double2> back(nvalid), ones(nvalid, make_double2(1.0 / (double)M, 0));
+  PassArgs d = a;
+  d.in = work.data();
+  d.out = back.data();
+  d.in_bstride = M;
+  d.out_bstride = nvalid;
+  d.nvalid_in = M;
+  d.nvalid_out = nvalid;
+  d.diag = ones.data();
+  emulate<AX_COL, M1, 2, 64, PROG_STOREDIAG, 1>(d, M2, 1);
+  double e2 = 0;
+  for (long long j = 0; j < nvalid; ++j) e2 = std::max(e2, (double)std::abs(cld(back[j].x, back[j].y) - xv[j]));
+  char buf[96];
+  std::snprintf(buf, sizeof buf, "pfa %dx%d nvalid=%lld fwd", M1, M2, nvalid);
+  check(buf, e / mx, 1e-14);
+  std::snprintf(buf, sizeof buf, "pfa %dx%d nvalid=%lld round trip", M1, M2, nvalid);
+  check(buf, e2, 1e-14);
+}
+
 int main(int argc, char** argv) {
   if (argc > 1 && std::string(argv[1]) == "c1") {
     const long long M1 = 1215, M2 = 1728, M = M1 * M2;
@@ -267,6 +424,7 @@ int main(int argc, char** argv) {
     std::vector<double2> buf(M, make_double2(1.0, 0.5)), inN(N, make_double2(0.5, 0.25)), dN(N, make_double2(1, 0));
     Tables t1;
     t1.build(M1, M);
+    t1.template build_plan<M1>();
     PassArgs a{};
     a.in = inN.data();
     a.out = buf.data();
@@ -288,6 +446,16 @@ int main(int argc, char** argv) {
     std::printf("c1 col entry emulated ok %f\n", buf[12345].x);
     return 0;
   }
+  if (argc > 1 && std::string(argv[1]) == "v2") {
+    test_double_v2<AX_ROW, 1728, 1, 192, -1>(2, 3000, 0, 0);
+    test_double_v2<AX_COL, 1215, 2, 288, 1>(5, 2000, 1, 1);
+    test_double_v2<AX_ROW, 64, 4, 64, 1>(6, 300, 0, 0);
+    test_double_v2<AX_COL, 256, 4, 128, -1>(6, 900, 1, 1);
+    test_double_v2<AX_ROW, 4096, 1, 256, 1>(1, 3000, 0, 0);
+    test_double_v2<AX_COL, 720, 2, 160, 1>(3, 1500, 1, 0);
+    std::printf(g_fail ? "SOME FAILED\n" : "ALL OK\n");
+    return g_fail;
+  }
   if (argc > 1) {
     test_lines<AX_COL, 1215, 2, 256, -1>(4);
     test_lines<AX_COL, 1215, 2, 256, 1>(3);
@@ -304,6 +472,7 @@ int main(int argc, char** argv) {
   test_dft<12, -1>(); test_dft<15, -1>(); test_dft<16, -1>(); test_dft<18, 1>();
   test_dft<20, 1>(); test_dft<24, 1>(); test_dft<27, 1>(); test_dft<32, 1>();
   test_dft<3, 1>(); test_dft<5, 1>(); test_dft<9, 1>(); test_dft<16, 1>();
+  test_dft<7, -1>(); test_dft<7, 1>(); test_dft<14, 1>(); test_dft<21, -1>(); test_dft<28, 1>();
   test_lines<AX_ROW, 1728, 1, 128, -1>(3);
   test_lines<AX_ROW, 720, 2, 128, 1>(4);
   test_lines<AX_COL, 1215, 2, 128, -1>(4);
@@ -316,6 +485,11 @@ int main(int argc, char** argv) {
   test_double<AX_COL, 12, 2, 32, 1>(4, 30);
   test_fourstep<12, 10>(61);
   test_fourstep<96, 90>(4099);
+  test_pfa<9, 16>(70);
+  test_pfa<27, 64>(800);
+  test_pfa<64, 135>(4099);
+  test_lines<AX_COL, 1029, 2, 160, -1>(3);
+  test_double<AX_ROW, 1029, 1, 160, 1>(2, 1500);
   std::printf(g_fail ? "SOME FAILED\n" : "ALL OK\n");
   return g_fail;
 }

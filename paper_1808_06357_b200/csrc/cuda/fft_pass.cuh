@@ -11,10 +11,16 @@
 // the four-step twiddles (ROW: IFFT x V FFT, COL: FFT x D IFFT).
 //
 // Each stage is a radix-R Stockham step (in-register DFT_R, twiddles from a
-// correctly rounded table, one in-place shared-memory exchange). The first
-// stage of the first transform reads straight from global memory and the last
-// stage of the last transform writes straight to global memory, so a pass
-// touches each element of the state exactly once in each direction.
+// correctly rounded table, one in-place shared-memory exchange).
+//
+// Two kernel shapes share the stage code:
+//  fft_pass_kernel  (v1): one CTA per tile of B lines; stage 0 loads straight
+//                   from global, the last stage stores straight to global.
+//  fft_pass2_kernel (v2, the hot PROG_DOUBLE + complex-diag passes):
+//                   persistent CTAs; tile t+1's lines and its diagonal-table
+//                   tile are prefetched with cp.async into a second shared
+//                   buffer while tile t is transformed, so the L2/HBM latency
+//                   is off the critical path.
 #pragma once
 
 #include "fft_core.cuh"
@@ -42,71 +48,142 @@ struct PassArgs {
   int pre_tw, post_tw, tw_shift;           // four-step twiddle exp(-2 pi i t / M)
   const double2* tw_lo;
   const double2* tw_hi;
-  const double2* fft_tw;                   // exp(-2 pi i t / L), t < L
+  const double2* fft_tw;                   // per-stage twiddles, Plan<L>::tw_offset layout
+  int nblk;                                // v2: line blocks per batch member
+  int ntiles;                              // v2: nblk * batch
+  // Good-Thomas (prime-factor) rank-1 layout: position (n1, n2) of the
+  // M1 x M2 view holds natural index (M2*n1 + M1*n2) mod M, gcd(M1,M2)=1.
+  int pfa;
+  int pM1, pM2;
+  long long pM;
 };
 
+// Shared-memory slots of one tile: B lines, each Plan<L>::phys-swizzled and
+// padded so that B adjacent lines accessed "line-fastest" hit distinct banks.
 template <int L, int B> struct SmemGeom {
+  static constexpr int span = Plan<L>::phys(L - 1) + 1;
   static constexpr int pad() {
     if (B == 1) return 0;
     int want = B == 2 ? 4 : (B == 4 ? 2 : 1);
-    return ((want - L % 8) % 8 + 8) % 8;
+    return ((want - span % 8) % 8 + 8) % 8;
   }
-  static constexpr int LS = L + pad();
+  static constexpr int LS = span + pad();
   static constexpr int bytes = B * LS * 16;
 };
 
 template <int AXIS, int L, int B, int PROG> struct Ctx {
   double2* sm;
-  const PassArgs* a;
+  PassArgs a;  // by value: fields resolve to parameter-bank operands, not pointer loads
   int line0;
   long long bat;
+  const double2* dgt = nullptr;  // v2: shared-memory diag tile (b*L + i)
 
-  LD_HD long long nat(int b, int i) const {
+  static constexpr int LS = SmemGeom<L, B>::LS;
+  LD_HD static int slot(int b, int i) { return b * LS + Plan<L>::phys(i); }
+
+  // array position of element (b, i) in the 2-D view
+  LD_HD long long pos(int b, int i) const {
     if (AXIS == AX_ROW) return (long long)(line0 + b) * L + i;
-    return (long long)i * a->ncols + (line0 + b);
+    return (long long)i * a.ncols + (line0 + b);
   }
+  // natural (sample / coefficient) index of element (b, i)
+  LD_HD long long nat(int b, int i) const {
+    if (AXIS == AX_COL && a.pfa) {
+      long long n = (long long)a.pM2 * i + (long long)a.pM1 * (line0 + b);
+      return n >= a.pM ? n - a.pM : n;
+    }
+    return pos(b, i);
+  }
+  // the compact (natural-order) side of single-transform programs
+  LD_HD long long in_index(int b, int i) const { return PROG == PROG_LOADDIAG ? nat(b, i) : pos(b, i); }
+  LD_HD long long out_index(int b, int i) const { return PROG == PROG_STOREDIAG ? nat(b, i) : pos(b, i); }
   LD_HD double2 twid(long long t) const {
-    const long long mask = (1LL << a->tw_shift) - 1;
-    return c_mul(a->tw_hi[t >> a->tw_shift], a->tw_lo[t & mask]);
+    const long long mask = (1LL << a.tw_shift) - 1;
+    return c_mul(a.tw_hi[t >> a.tw_shift], a.tw_lo[t & mask]);
   }
   LD_HD long long tw_index(int b, int i) const { return (long long)(line0 + b) * i; }
   LD_HD double2 apply_diag(double2 v, long long j) const {
-    switch (a->diag_kind) {
-      case DG_CPLX: return c_mul(v, a->diag[j]);
-      case DG_LUT16: return c_mul(v, a->lut[((const unsigned short*)a->diag_idx)[j]]);
-      case DG_LUT8: return c_mul(v, a->lut[((const unsigned char*)a->diag_idx)[j]]);
-      case DG_SCALAR: return c_mul(v, a->lut[0]);
+    switch (a.diag_kind) {
+      case DG_CPLX: return c_mul(v, a.diag[j]);
+      case DG_LUT16: return c_mul(v, a.lut[((const unsigned short*)a.diag_idx)[j]]);
+      case DG_LUT8: return c_mul(v, a.lut[((const unsigned char*)a.diag_idx)[j]]);
+      case DG_SCALAR: return c_mul(v, a.lut[0]);
       default: return v;
     }
   }
-  LD_HD bool live(int b) const { return line0 + b < a->nlines; }
+  LD_HD bool live(int b) const { return line0 + b < a.nlines; }
+  // v1 stage-0 source: global memory
   LD_HD double2 gload(int b, int i) const {
-    long long j = nat(b, i);
+    long long j = in_index(b, i);
     double2 v = make_double2(0.0, 0.0);
     if (!live(b)) return v;
-    if (j < a->nvalid_in) {
-      v = a->in[bat * a->in_bstride + j];
+    if (j < a.nvalid_in) {
+      v = a.in[bat * a.in_bstride + j];
       if (PROG == PROG_LOADDIAG) v = apply_diag(v, j);  // diag tables hold nvalid_in entries
     }
-    if (AXIS == AX_COL && a->pre_tw) v = c_mulc(v, twid(tw_index(b, i)));
+    return v;
+  }
+  // v2 stage-0 source: the prefetched tile (masked entries were zero-filled)
+  LD_HD double2 tload(int b, int i) const {
+    double2 v = sm[slot(b, i)];
+    if (PROG == PROG_LOADDIAG) {
+      long long j = in_index(b, i);
+      if (live(b) && j < a.nvalid_in) v = apply_diag(v, j);
+    }
     return v;
   }
   LD_HD void gstore(int b, int i, double2 v) const {
     if (!live(b)) return;
-    if (AXIS == AX_COL && a->post_tw) v = c_mul(v, twid(tw_index(b, i)));
-    long long j = nat(b, i);
-    if (j >= a->nvalid_out) return;
+    long long j = out_index(b, i);
+    if (j >= a.nvalid_out) return;
     if (PROG == PROG_STOREDIAG) v = apply_diag(v, j);
-    a->out[bat * a->out_bstride + j] = v;
+    a.out[bat * a.out_bstride + j] = v;
   }
+  // the mid diagonal and its mask are indexed by array position
   LD_HD double2 mid(int b, int i, double2 v) const {
-    long long j = nat(b, i);
-    if (!live(b) || j >= a->nvalid_mid) return make_double2(0.0, 0.0);
+    long long j = pos(b, i);
+    if (!live(b) || j >= a.nvalid_mid) return make_double2(0.0, 0.0);
+    if (dgt) return c_mul(v, dgt[b * L + i]);
     return apply_diag(v, j);
   }
 };
 
-enum : int { SRC_SMEM = 0, SRC_GLOBAL = 1 };
+LD_HD double2 __ldg_d2(const double2* p) {
+#if defined(__CUDA_ARCH__)
+  return __ldg(p);
+#else
+  return *p;
+#endif
+}
+
+// Powers w^r, 0 <= r < R, of a twiddle from correctly rounded bases
+// w, w^4, w^16: every power is at most three products deep.
+template <int R> struct Pow {
+  double2 b1, b2, b3, b4, b8, b12, b16;
+  LD_HD void init(double2 w1, double2 w4, double2 w16) {
+    b1 = w1;
+    b2 = c_mul(w1, w1);
+    b3 = c_mul(b2, w1);
+    b4 = w4;
+    b8 = c_mul(w4, w4);
+    b12 = c_mul(b8, w4);
+    b16 = w16;
+  }
+  template <int r> LD_HD double2 get() const {
+    if constexpr (r == 0) return make_double2(1.0, 0.0);
+    else if constexpr (r == 1) return b1;
+    else if constexpr (r == 2) return b2;
+    else if constexpr (r == 3) return b3;
+    else if constexpr (r == 4) return b4;
+    else if constexpr (r == 8) return b8;
+    else if constexpr (r == 12) return b12;
+    else if constexpr (r == 16) return b16;
+    else if constexpr (r < 16) return c_mul(get<4 * (r / 4)>(), get<r % 4>());
+    else return c_mul(b16, get<r - 16>());
+  }
+};
+
+enum : int { SRC_SMEM = 0, SRC_GLOBAL = 1, SRC_TILE = 2 };
 enum : int { DST_SMEM = 0, DST_SMEM_MID = 1, DST_GLOBAL = 2 };
 
 template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, int DST> struct Stage {
@@ -116,7 +193,6 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
   static constexpr int T = L / R;
   static constexpr int TASKS = B * T;
   static constexpr int TPT = (TASKS + NT - 1) / NT;
-  static constexpr int LS = SmemGeom<L, B>::LS;
   static constexpr int src = SRC, dst = DST, nt = NT;
   using C = Ctx<AXIS, L, B, PROG>;
 
@@ -129,6 +205,20 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
       j = q / B;
     }
   }
+  // four-step twiddles W(col * (j + r*T)) = W(col*j) * W(col*T)^r for the
+  // elements j + r*T a task touches in stage 0 / the last stage
+  LD_HD static void fourstep(const C& c, int b, int j, double2 (&v)[R], bool conj) {
+    const long long col = c.line0 + b;
+    const double2 base = c.twid(col * j);
+    Pow<R> pw;
+    pw.init(c.twid(col * T), R > 4 ? c.twid(col * 4 * T) : make_double2(1.0, 0.0),
+            R > 16 ? c.twid(col * 16 * T) : make_double2(1.0, 0.0));
+    sfor<R>([&](auto rc) {
+      constexpr int r = decltype(rc)::value;
+      const double2 w = r == 0 ? base : c_mul(base, pw.template get<r>());
+      v[r] = conj ? c_mulc(v[r], w) : c_mul(v[r], w);
+    });
+  }
   LD_HD static void read(const C& c, int tid, double2 (&v)[TPT][R]) {
 #pragma unroll
     for (int t = 0; t < TPT; ++t) {
@@ -140,9 +230,12 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
       for (int r = 0; r < R; ++r) {
         if (SRC == SRC_GLOBAL)
           v[t][r] = c.gload(b, j + r * T);
+        else if (SRC == SRC_TILE)
+          v[t][r] = c.tload(b, j + r * T);
         else
-          v[t][r] = c.sm[b * LS + j + r * T];
+          v[t][r] = c.sm[C::slot(b, j + r * T)];
       }
+      if (SRC != SRC_SMEM && AXIS == AX_COL && c.a.pre_tw) fourstep(c, b, j, v[t], true);
     }
   }
   LD_HD static void write(const C& c, int tid, double2 (&v)[TPT][R]) {
@@ -154,24 +247,32 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
       map(q, b, j);
       const int k = j % Ns;
       if (Ns > 1) {
-        const int step = L / (Ns * R);
-#pragma unroll
-        for (int r = 1; r < R; ++r) {
-          double2 w = c.a->fft_tw[r * k * step];
-          v[t][r] = SIGN < 0 ? c_mul(v[t][r], w) : c_mulc(v[t][r], w);
-        }
+        // stage twiddles w^r from table rows r = 1, 4, 16
+        const double2* tw = c.a.fft_tw + P::tw_offset(S) + k;
+        Pow<R> pw;
+        pw.init(__ldg_d2(tw), R > 4 ? __ldg_d2(tw + 3 * Ns) : make_double2(1.0, 0.0),
+                R > 16 ? __ldg_d2(tw + 15 * Ns) : make_double2(1.0, 0.0));
+        sfor<R>([&](auto rc) {
+          constexpr int r = decltype(rc)::value;
+          if constexpr (r > 0) {
+            const double2 w = pw.template get<r>();
+            v[t][r] = SIGN < 0 ? c_mul(v[t][r], w) : c_mulc(v[t][r], w);
+          }
+        });
       }
       DFT<R, SIGN>::run(v[t]);
       const int idxD = (j / Ns) * Ns * R + k;
+      // last stage: idxD == j, outputs at j + r*T (the four-step pattern)
+      if (DST == DST_GLOBAL && AXIS == AX_COL && c.a.post_tw) fourstep(c, b, j, v[t], false);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         int pos = idxD + r * Ns;
         if (DST == DST_GLOBAL)
           c.gstore(b, pos, v[t][r]);
         else if (DST == DST_SMEM_MID)
-          c.sm[b * LS + pos] = c.mid(b, pos, v[t][r]);
+          c.sm[C::slot(b, pos)] = c.mid(b, pos, v[t][r]);
         else
-          c.sm[b * LS + pos] = v[t][r];
+          c.sm[C::slot(b, pos)] = v[t][r];
       }
     }
   }
@@ -182,7 +283,7 @@ struct DevExec {
   template <class St, class C> __device__ __forceinline__ static void stage(const C& c) {
     double2 v[St::TPT][St::R];
     St::read(c, threadIdx.x, v);
-    if (St::src == SRC_SMEM) __syncthreads();
+    if (St::src != SRC_GLOBAL) __syncthreads();  // in place: all reads before any write
     St::write(c, threadIdx.x, v);
     if (St::dst != DST_GLOBAL) __syncthreads();
   }
@@ -203,22 +304,92 @@ LD_HD void run_fft(const C& c) {
 }
 
 #pragma nv_exec_check_disable
-template <class Exec, int AXIS, int L, int B, int NT, int PROG, int SIGN1>
+template <class Exec, int AXIS, int L, int B, int NT, int PROG, int SIGN1, int FIRST = SRC_GLOBAL>
 LD_HD void run_pass(const Ctx<AXIS, L, B, PROG>& c) {
   if constexpr (PROG == PROG_DOUBLE) {
-    run_fft<Exec, AXIS, L, B, NT, PROG, SIGN1, SRC_GLOBAL, DST_SMEM_MID>(c);
+    run_fft<Exec, AXIS, L, B, NT, PROG, SIGN1, FIRST, DST_SMEM_MID>(c);
     run_fft<Exec, AXIS, L, B, NT, PROG, -SIGN1, SRC_SMEM, DST_GLOBAL>(c);
   } else {
-    run_fft<Exec, AXIS, L, B, NT, PROG, SIGN1, SRC_GLOBAL, DST_GLOBAL>(c);
+    run_fft<Exec, AXIS, L, B, NT, PROG, SIGN1, FIRST, DST_GLOBAL>(c);
   }
 }
 
+// ------------------------------------------------------------ tile loads
+// Element (b, i) of a tile: global offset and validity, in the order the
+// copy loop walks it (ROW: along the line; COL: B adjacent columns first, so
+// each global row segment of B*16 bytes is read by consecutive threads).
+template <int AXIS, int L, int B> struct TileWalk {
+  LD_HD static void elem(int q, int& b, int& i) {
+    if (AXIS == AX_ROW) {
+      b = q / L;
+      i = q % L;
+    } else {
+      b = q % B;
+      i = q / B;
+    }
+  }
+};
+
 #if defined(__CUDACC__)
-template <int AXIS, int L, int B, int NT, int PROG, int SIGN1>
-__global__ void __launch_bounds__(NT) fft_pass_kernel(const __grid_constant__ PassArgs a) {
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <int AXIS, int L, int B, int NT, int PROG>
+__device__ __forceinline__ void load_tile(const PassArgs& a, double2* buf, double2* dg, int line0, long long bat) {
+  using C = Ctx<AXIS, L, B, PROG>;
+  for (int q = threadIdx.x; q < B * L; q += NT) {
+    int b, i;
+    TileWalk<AXIS, L, B>::elem(q, b, i);
+    const bool live = line0 + b < a.nlines;
+    // PROG_DOUBLE tiles: work buffer and diag table are both in position order
+    const long long j = AXIS == AX_ROW ? (long long)(line0 + b) * L + i : (long long)i * a.ncols + (line0 + b);
+    const bool ok = live && j < a.nvalid_in;
+    cp_async16(buf + C::slot(b, i), ok ? (const void*)(a.in + bat * a.in_bstride + j) : (const void*)a.in, ok ? 16 : 0);
+    if (dg) {
+      const bool okd = live && j < a.nvalid_mid;
+      cp_async16(dg + b * L + i, okd ? (const void*)(a.diag + j) : (const void*)a.diag, okd ? 16 : 0);
+    }
+  }
+}
+#endif
+
+#if defined(__CUDACC__)
+template <int AXIS, int L, int B, int NT, int PROG, int SIGN1, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) fft_pass_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ double2 lattdse_smem[];
-  Ctx<AXIS, L, B, PROG> c{lattdse_smem, &a, (int)blockIdx.x * B, (long long)blockIdx.y};
+  Ctx<AXIS, L, B, PROG> c{lattdse_smem, a, (int)blockIdx.x * B, (long long)blockIdx.y};
   run_pass<DevExec, AXIS, L, B, NT, PROG, SIGN1>(c);
+}
+
+// v2: persistent, double-buffered. Only PROG_DOUBLE with a complex diagonal
+// table (the per-step passes). Shared memory: 2 data tiles + 2 diag tiles.
+template <int AXIS, int L, int B, int NT, int SIGN1>
+__global__ void __launch_bounds__(NT) fft_pass2_kernel(const __grid_constant__ PassArgs a) {
+  extern __shared__ double2 lattdse_smem[];
+  constexpr int TS = B * SmemGeom<L, B>::LS;
+  double2* data[2] = {lattdse_smem, lattdse_smem + TS};
+  double2* dg[2] = {lattdse_smem + 2 * TS, lattdse_smem + 2 * TS + B * L};
+  int t = blockIdx.x;
+  if (t >= a.ntiles) return;
+  auto line0_of = [&](int tt) { return (tt % a.nblk) * B; };
+  auto bat_of = [&](int tt) { return (long long)(tt / a.nblk); };
+  load_tile<AXIS, L, B, NT, PROG_DOUBLE>(a, data[0], dg[0], line0_of(t), bat_of(t));
+  cp_async_commit();
+  int cur = 0;
+  for (; t < a.ntiles; t += gridDim.x) {
+    cp_async_wait_all();
+    __syncthreads();  // tile t landed; every thread is done with tile t-1's buffers
+    const int tn = t + gridDim.x;
+    if (tn < a.ntiles) load_tile<AXIS, L, B, NT, PROG_DOUBLE>(a, data[cur ^ 1], dg[cur ^ 1], line0_of(tn), bat_of(tn));
+    cp_async_commit();
+    Ctx<AXIS, L, B, PROG_DOUBLE> c{data[cur], a, line0_of(t), bat_of(t), dg[cur]};
+    run_pass<DevExec, AXIS, L, B, NT, PROG_DOUBLE, SIGN1, SRC_TILE>(c);
+    cur ^= 1;
+  }
 }
 #endif
 

@@ -10,11 +10,13 @@ namespace lattdse::dev {
 //  ROW lines are contiguous: one line per CTA for L >= 256, else several.
 //  COL lines are strided: B adjacent columns per CTA so every row segment a
 //  CTA touches is B*16 bytes (>= one 32-byte sector).
+// NT covers the busiest stage (B * L / R_min tasks) so no thread loops.
 template <int AXIS, int L> struct Geometry {
   static constexpr int B = AXIS == lattdse_dev::AX_ROW ? (L >= 256 ? 1 : 256 / L)
-                                                       : (L >= 1024 ? 2 : (L >= 256 ? 4 : 8));
-  static constexpr int raw = B * L / 8;
-  static constexpr int NT = raw <= 32 ? 32 : (raw >= 256 ? 256 : ((raw + 31) / 32) * 32);
+                                                       : (L >= 512 ? 2 : (L >= 128 ? 4 : 8));
+  static constexpr int raw = B * lattdse_dev::Plan<L>::max_tasks();
+  static constexpr int NT = raw <= 32 ? 32 : (raw >= 512 ? 512 : ((raw + 31) / 32) * 32);
+  static constexpr int smem2 = 2 * lattdse_dev::SmemGeom<L, B>::bytes + 2 * B * L * 16;
 };
 
 template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
@@ -24,6 +26,21 @@ template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
   k.B = G::B;
   k.NT = G::NT;
   k.smem = lattdse_dev::SmemGeom<L, G::B>::bytes;
+  k.nst = lattdse_dev::Plan<L>::nst;
+  for (int s = 0; s < k.nst && s < 16; ++s) k.radix[s] = lattdse_dev::Plan<L>::radix(s);
+  if constexpr (PROG == lattdse_dev::PROG_DOUBLE) {
+    k.fn_mb[1] = k.fn;
+    k.fn_mb[2] = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN, 2>);
+    k.fn_mb[3] = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN, 3>);
+    k.fn_mb[4] = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN, 4>);
+    // measured on C1 (profiles/README.md): 3 resident CTAs/SM balance register
+    // caps (small L1-resident spills) against occupancy for 5-10 warp CTAs
+    k.default_mb = G::NT <= 320 ? 3 : (G::NT <= 512 ? 2 : 1);
+  }
+  if constexpr (PROG == lattdse_dev::PROG_DOUBLE && G::smem2 <= 227 * 1024) {
+    k.fn2 = reinterpret_cast<const void*>(&lattdse_dev::fft_pass2_kernel<AXIS, L, G::B, G::NT, SIGN>);
+    k.smem2 = G::smem2;
+  }
   register_pass_kernel(AXIS, L, PROG, SIGN, k);
 }
 

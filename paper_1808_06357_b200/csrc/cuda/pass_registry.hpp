@@ -8,13 +8,26 @@
 
 namespace lattdse::dev {
 
+
 struct PassKernel {
   const void* fn = nullptr;  // __global__ fft_pass_kernel<...>
   int B = 0;                 // lines per CTA
   int NT = 0;                // threads per CTA
   int smem = 0;              // dynamic shared memory bytes
   bool attr_set = false;     // cudaFuncAttributeMaxDynamicSharedMemorySize applied
+  // v2 persistent double-buffered variant (PROG_DOUBLE with a complex diag)
+  const void* fn2 = nullptr;
+  int smem2 = 0;
+  bool attr2_set = false;
+  int blocks_per_sm2 = 0;
+  // PROG_DOUBLE instantiated with __launch_bounds__(NT, minBlocks) for
+  // minBlocks = 1..4 (register cap vs occupancy); index 0 unused
+  const void* fn_mb[5] = {};
+  int default_mb = 1;
+  int nst = 0;
+  int radix[16] = {};        // Plan<L> radices, stage order
 };
+
 
 PassKernel* find_pass_kernel(int axis, int L, int prog, int sign);
 void register_pass_kernel(int axis, int L, int prog, int sign, const PassKernel& k);

@@ -122,6 +122,29 @@ __global__ void k_wrap(const double2* __restrict__ k, long long N, long long M, 
   }
 }
 
+// Good-Thomas position p = n1*M2 + n2 holds natural n = (M2 n1 + M1 n2) mod M.
+__device__ __forceinline__ long long pfa_nat(long long p, long long M1, long long M2, long long M) {
+  const long long n1 = p / M2, n2 = p - n1 * M2;
+  long long n = M2 * n1 + M1 * n2;
+  return n >= M ? n - M : n;
+}
+__global__ void k_perm_c(const double2* __restrict__ v, long long N, long long M1, long long M2,
+                         double2* __restrict__ out) {
+  const long long M = M1 * M2;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < M; p += (long long)gridDim.x * blockDim.x) {
+    const long long n = pfa_nat(p, M1, M2, M);
+    out[p] = n < N ? v[n] : make_double2(0.0, 0.0);
+  }
+}
+__global__ void k_perm_u16(const unsigned short* __restrict__ v, long long N, long long M1, long long M2,
+                           unsigned short sentinel, unsigned short* __restrict__ out) {
+  const long long M = M1 * M2;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < M; p += (long long)gridDim.x * blockDim.x) {
+    const long long n = pfa_nat(p, M1, M2, M);
+    out[p] = n < N ? v[n] : sentinel;
+  }
+}
+
 __global__ void k_lut_gather(const unsigned short* __restrict__ idx, const double2* __restrict__ lut, long long n,
                              double2* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -208,6 +231,7 @@ struct Solver::Impl {
   // transform geometry
   long long M = 0, M1 = 0, M2 = 0;  // work = M1 rows x M2 cols
   int tw_shift = 0;
+  bool pfa = false;                 // Good-Thomas layout (rank-1), else four-step
 
   // device
   int device = 0;
@@ -215,7 +239,8 @@ struct Solver::Impl {
   DBuf<double2> work, samples, coef, tmp;
   DBuf<double> v;                 // potential at the points
   DBuf<unsigned short> nidx;      // ||h_chi||^2 per chi
-  DBuf<double2> V, Vh, Ventry, Vexit, kin_lut, kin_full;
+  DBuf<double2> V, Vh, Ventry, Vexit, kin_lut, kin_full, Vperm;
+  DBuf<unsigned short> nidx_perm;  // Good-Thomas: norm index in position order (sentinel = zero phase)
   DBuf<double2> Khat, B1hat, B2hat, chirp, chirp_c, chirp_n;
   DBuf<double2> tw_col, tw_row, tw_lo, tw_hi, scal;
   DBuf<double> partial;
@@ -223,6 +248,9 @@ struct Solver::Impl {
   bool bluestein_tables = false;
   long long launches = 0;
   bool sync_check = std::getenv("LATTDSE_SYNC_CHECK") != nullptr;  // debug: sync after every launch
+  bool use_v2 = std::getenv("LATTDSE_PASS_V2") != nullptr;           // persistent double-buffered passes (opt-in)
+  int num_sms = 148;
+  int minb_override = std::getenv("LATTDSE_MINB") ? std::atoi(std::getenv("LATTDSE_MINB")) : 0;
 
   explicit Impl(const Lattice& l) : lat(l) {}
 
@@ -230,32 +258,44 @@ struct Solver::Impl {
   void launch_pass(int axis, int L, int prog, int sign, PassArgs a, long long nlines, long long nbatch) {
     dev::PassKernel* k = dev::find_pass_kernel(axis, L, prog, sign);
     if (!k) raise(Errc::unsupported, "no pass kernel compiled for axis " + std::to_string(axis) + " L=" + std::to_string(L));
-    if (!k->attr_set) {
-      LD_CK(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem));
-      k->attr_set = true;
-    }
     a.nlines = (int)nlines;
-    dim3 grid((unsigned)((nlines + k->B - 1) / k->B), (unsigned)nbatch);
+    const bool v2 = use_v2 && k->fn2 && prog == PROG_DOUBLE && a.diag_kind == DG_CPLX;
+    const void* fn = v2 ? k->fn2 : k->fn;
+    if (!v2 && prog == PROG_DOUBLE) {
+      const int mb = minb_override > 0 ? minb_override : k->default_mb;
+      if (mb >= 1 && mb <= 4 && k->fn_mb[mb]) fn = k->fn_mb[mb];
+    }
+    int smem = v2 ? k->smem2 : k->smem;
+    dim3 grid;
+    if (v2) {
+      if (!k->attr2_set) {
+        LD_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        LD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k->blocks_per_sm2, fn, k->NT, smem));
+        k->attr2_set = true;
+      }
+      a.nblk = (int)((nlines + k->B - 1) / k->B);
+      a.ntiles = (int)(a.nblk * nbatch);
+      const long long resident = (long long)std::max(1, k->blocks_per_sm2) * num_sms;
+      grid = dim3((unsigned)std::min<long long>(a.ntiles, resident), 1);
+    } else {
+      if (!k->attr_set) {
+        for (int m = 0; m <= 4; ++m) {
+          const void* f = m == 0 ? k->fn : k->fn_mb[m];
+          if (f) LD_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        }
+        k->attr_set = true;
+      }
+      grid = dim3((unsigned)((nlines + k->B - 1) / k->B), (unsigned)nbatch);
+    }
     void* args[] = {&a};
-    LD_CK(cudaLaunchKernel(k->fn, grid, dim3(k->NT), args, (size_t)k->smem, stream));
+    LD_CK(cudaLaunchKernel(fn, grid, dim3(k->NT), args, (size_t)smem, stream));
     ++launches;
     if (sync_check) {
       cudaError_t e = cudaStreamSynchronize(stream);
-      if (e != cudaSuccess) {
-        std::fprintf(stderr,
-                     "pass fault: in=%p out=%p bstr=%lld/%lld nvalid=%lld/%lld/%lld ncols=%d nlines=%d dk=%d diag=%p "
-                     "idx=%p lut=%p tw=%d/%d/%d lo=%p hi=%p fft_tw=%p | work=%p(%zu) M=%lld M1=%lld M2=%lld N=%lld "
-                     "twcol=%p(%zu) twrow=%p(%zu) lo=%p(%zu) hi=%p(%zu) B1=%p B2=%p K=%p\n",
-                     (const void*)a.in, (void*)a.out, a.in_bstride, a.out_bstride, a.nvalid_in, a.nvalid_mid,
-                     a.nvalid_out, a.ncols, a.nlines, a.diag_kind, (const void*)a.diag, a.diag_idx, (const void*)a.lut,
-                     a.pre_tw, a.post_tw, a.tw_shift, (const void*)a.tw_lo, (const void*)a.tw_hi,
-                     (const void*)a.fft_tw, (void*)work.p, work.n, M, M1, M2, N, (void*)tw_col.p, tw_col.n,
-                     (void*)tw_row.p, tw_row.n, (void*)tw_lo.p, tw_lo.n, (void*)tw_hi.p, tw_hi.n, (void*)B1hat.p,
-                     (void*)B2hat.p, (void*)Khat.p);
+      if (e != cudaSuccess)
         raise(Errc::device_error, "pass axis=" + std::to_string(axis) + " L=" + std::to_string(L) + " prog=" +
-                                      std::to_string(prog) + " sign=" + std::to_string(sign) + " grid=" +
-                                      std::to_string(grid.x) + "x" + std::to_string(grid.y) + ": " + cudaGetErrorString(e));
-      }
+                                      std::to_string(prog) + " sign=" + std::to_string(sign) + (v2 ? " v2" : " v1") +
+                                      ": " + cudaGetErrorString(e));
     }
   }
   int grid1d(long long n) const { return (int)std::min<long long>((n + 255) / 256, 148 * 16); }
@@ -275,6 +315,10 @@ struct Solver::Impl {
     a.tw_hi = tw_hi.p;
     a.fft_tw = axis == AX_COL ? tw_col.p : tw_row.p;
     a.ncols = (int)M2;
+    a.pfa = pfa ? 1 : 0;
+    a.pM1 = (int)M1;
+    a.pM2 = (int)M2;
+    a.pM = M;
     return a;
   }
   static void set_diag(PassArgs& a, const double2* d) {
@@ -292,19 +336,21 @@ struct Solver::Impl {
     a.out_bstride = M;
     a.nvalid_in = N;
     a.nvalid_mid = a.nvalid_out = M;
-    a.post_tw = 1;
+    a.post_tw = pfa ? 0 : 1;
     set_diag(a, diag);
     launch_pass(AX_COL, (int)M1, PROG_LOADDIAG, -1, a, M2, nb);
   }
+  // x V at the mid: four-step -> natural V masked at N; Good-Thomas -> the
+  // position-ordered V_perm with the mask folded in (zeros)
   void r1_col_mid(double2* w, const double2* diag, long long nb) {
     PassArgs a = base_args(AX_COL);
     a.in = w;
     a.out = w;
     a.in_bstride = a.out_bstride = M;
     a.nvalid_in = a.nvalid_out = M;
-    a.nvalid_mid = N;
-    a.pre_tw = a.post_tw = 1;
-    set_diag(a, diag);
+    a.nvalid_mid = pfa ? M : N;
+    a.pre_tw = a.post_tw = pfa ? 0 : 1;
+    set_diag(a, pfa ? Vperm.p : diag);
     launch_pass(AX_COL, (int)M1, PROG_DOUBLE, +1, a, M2, nb);
   }
   void r1_col_mid_lut(double2* w, long long nb) {  // x D/N through the norm index
@@ -313,10 +359,10 @@ struct Solver::Impl {
     a.out = w;
     a.in_bstride = a.out_bstride = M;
     a.nvalid_in = a.nvalid_out = M;
-    a.nvalid_mid = N;
-    a.pre_tw = a.post_tw = 1;
+    a.nvalid_mid = pfa ? M : N;
+    a.pre_tw = a.post_tw = pfa ? 0 : 1;
     a.diag_kind = DG_LUT16;
-    a.diag_idx = nidx.p;
+    a.diag_idx = pfa ? nidx_perm.p : nidx.p;
     a.lut = kin_lut.p;
     launch_pass(AX_COL, (int)M1, PROG_DOUBLE, +1, a, M2, nb);
   }
@@ -328,7 +374,7 @@ struct Solver::Impl {
     a.out_bstride = out_stride;
     a.nvalid_in = a.nvalid_mid = M;
     a.nvalid_out = N;
-    a.pre_tw = 1;
+    a.pre_tw = pfa ? 0 : 1;
     set_diag(a, diag);
     launch_pass(AX_COL, (int)M1, PROG_STOREDIAG, +1, a, M2, nb);
   }
@@ -382,24 +428,34 @@ struct Solver::Impl {
       return;
     }
     const long long need = 2 * N - 1;
-    long long best = -1, b1 = 0, b2 = 0;
-    double bal = 0;
+    // best four-step (any factors) and best Good-Thomas (coprime) split
+    long long best = -1, b1 = 0, b2 = 0, bestp = -1, p1 = 0, p2 = 0;
+    double bal = 0, balp = 0;
+    auto better = [](long long m, double bl, int L1, long long cur, double curbal, long long curL1) {
+      return cur < 0 || m < cur || (m == cur && (bl < curbal - 1e-12 || (std::fabs(bl - curbal) <= 1e-12 && L1 < curL1)));
+    };
     for (int L1 : dev::pass_lengths(AX_COL))
       for (int L2 : dev::pass_lengths(AX_ROW)) {
         long long m = (long long)L1 * L2;
         if (m < need) continue;
         double bl = std::fabs(std::log((double)L1 / L2));
-        if (best < 0 || m < best || (m == best && (bl < bal - 1e-12 || (std::fabs(bl - bal) <= 1e-12 && L1 < b1)))) {
-          best = m;
-          b1 = L1;
-          b2 = L2;
-          bal = bl;
-        }
+        if (better(m, bl, L1, best, bal, b1)) { best = m; b1 = L1; b2 = L2; bal = bl; }
+        if (std::gcd(L1, L2) == 1 && better(m, bl, L1, bestp, balp, p1)) { bestp = m; p1 = L1; p2 = L2; balp = bl; }
       }
     if (best < 0) raise(Errc::unsupported, "N=" + std::to_string(N) + " exceeds the single-level four-step range");
-    M = best;
-    M1 = b1;
-    M2 = b2;
+    // Good-Thomas needs no four-step twiddles (opt-in until it beats the four-step path)
+    const bool allow_pfa = std::getenv("LATTDSE_PFA") != nullptr;  // opt-in: see DESIGN.md
+    if (allow_pfa && bestp > 0 && (double)bestp <= 1.03 * (double)best) {
+      pfa = true;
+      M = bestp;
+      M1 = p1;
+      M2 = p2;
+    } else {
+      pfa = false;
+      M = best;
+      M1 = b1;
+      M2 = b2;
+    }
   }
 
   void upload_twiddles() {
@@ -407,8 +463,16 @@ struct Solver::Impl {
       b.alloc(h.size());
       LD_CK(cudaMemcpyAsync(b.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
     };
-    up(tw_col, root_table(M1, M1, 1));
-    up(tw_row, root_table(M2, M2, 1));
+    auto stage_tw = [&](int axis, long long L) {
+      const dev::PassKernel* k = dev::find_pass_kernel(axis, (int)L, PROG_DOUBLE, -1);
+      if (!k) raise(Errc::unsupported, "no pass kernel for L=" + std::to_string(L));
+      const int n = std::max(1, build_stage_twiddles(k->radix, k->nst, nullptr));
+      std::vector<double2> t(n, make_double2(1.0, 0.0));
+      build_stage_twiddles(k->radix, k->nst, t.data());
+      return t;
+    };
+    up(tw_col, stage_tw(AX_COL, M1));
+    up(tw_row, stage_tw(AX_ROW, M2));
     tw_shift = 0;
     while ((1LL << (2 * tw_shift)) < M) ++tw_shift;
     const long long nlo = 1LL << tw_shift, nhi = (M + nlo - 1) / nlo;
@@ -429,21 +493,27 @@ struct Solver::Impl {
     // B1 = FFT_M(wrap conj c)/M (forward DFT), B2 = FFT_M(wrap c)/M (inverse)
     B1hat.alloc(M);
     B2hat.alloc(M);
-    k_wrap<<<grid1d(M), 256, 0, stream>>>(chirp_c.p, N, M, 1.0 / (double)M, 1, B1hat.p);
+    DBuf<double2> nat;
+    nat.alloc(M);
+    k_wrap<<<grid1d(M), 256, 0, stream>>>(chirp_c.p, N, M, 1.0 / (double)M, 1, nat.p);
     aux_done("k_wrap");
-    r1_fft_table_full(B1hat.p);
-    k_wrap<<<grid1d(M), 256, 0, stream>>>(chirp.p, N, M, 1.0 / (double)M, 1, B2hat.p);
+    r1_fft_table_full(nat.p, B1hat.p);
+    k_wrap<<<grid1d(M), 256, 0, stream>>>(chirp.p, N, M, 1.0 / (double)M, 1, nat.p);
     aux_done("k_wrap");
-    r1_fft_table_full(B2hat.p);
+    r1_fft_table_full(nat.p, B2hat.p);
+    LD_CK(cudaStreamSynchronize(stream));  // `nat` is freed at scope exit
     bluestein_tables = true;
   }
-  void r1_fft_table_full(double2* w) {
+  // K^ = FFT_M(K) with K in natural order in `src` (M entries), written in the
+  // ROW pass's position layout to `w`. src != w: the Good-Thomas gather reads
+  // natural positions owned by other CTAs, so it cannot run in place.
+  void r1_fft_table_full(const double2* src, double2* w) {
     PassArgs a = base_args(AX_COL);
-    a.in = w;
+    a.in = src;
     a.out = w;
     a.in_bstride = a.out_bstride = M;
     a.nvalid_in = a.nvalid_mid = a.nvalid_out = M;
-    a.post_tw = 1;
+    a.post_tw = pfa ? 0 : 1;
     launch_pass(AX_COL, (int)M1, PROG_LOADDIAG, -1, a, M2, 1);
     r1_row_fwd(w);
   }
@@ -481,7 +551,7 @@ struct Solver::Impl {
     k_phase<<<grid1d(N), 256, 0, stream>>>(v.p, N, -dt / (2.0 * eps), Vh.p);
     aux_done("k_phase");
     // kinetic LUT exp(-i eps dt 2 pi^2 s)/N for s = 0..max ||h||^2
-    std::vector<double2> lut(max_norm2 + 1);
+    std::vector<double2> lut(max_norm2 + 2, make_double2(0.0, 0.0));  // [max+1] = 0: masked slots
     for (std::uint32_t s = 0; s <= max_norm2; ++s) {
       long double a = -(long double)eps * (long double)dt * 2.0L * kPiL * kPiL * (long double)s;
       long double r = fmodl(a, 2.0L * kPiL);
@@ -491,6 +561,16 @@ struct Solver::Impl {
     LD_CK(cudaMemcpyAsync(kin_lut.p, lut.data(), lut.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
     LD_CK(cudaStreamSynchronize(stream));  // lut is a host temporary
 
+    if (rank == 1 && pfa) {
+      Vperm.alloc(M);
+      k_perm_c<<<grid1d(M), 256, 0, stream>>>(V.p, N, M1, M2, Vperm.p);
+      aux_done("k_perm_c");
+      if (method == "bluestein" && !nidx_perm.p) {
+        nidx_perm.alloc(M);
+        k_perm_u16<<<grid1d(M), 256, 0, stream>>>(nidx.p, N, M1, M2, (unsigned short)(max_norm2 + 1), nidx_perm.p);
+        aux_done("k_perm_u16");
+      }
+    }
     if (rank == 1) {
       build_chirp_tables();
       if (method == "circulant") {
@@ -504,9 +584,9 @@ struct Solver::Impl {
         scratch.alloc(M);
         synthesize_dev(kin_full.p, tmp.p, scratch.p);
         Khat.alloc(M);
-        k_wrap<<<grid1d(M), 256, 0, stream>>>(tmp.p, N, M, 1.0 / (double)M, 0, Khat.p);
+        k_wrap<<<grid1d(M), 256, 0, stream>>>(tmp.p, N, M, 1.0 / (double)M, 0, scratch.p);
         aux_done("k_wrap");
-        r1_fft_table_full(Khat.p);
+        r1_fft_table_full(scratch.p, Khat.p);
         LD_CK(cudaStreamSynchronize(stream));
         kin_full.release();
         Ventry.release();
@@ -615,7 +695,7 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
     s.n2 = lat.moduli()[1];
   }
   if (aa.n_total != s.N) raise(Errc::spec_mismatch, "anti-aliasing set does not match the lattice");
-  if (aa.max_norm2 > 65535) raise(Errc::unsupported, "||h||^2 above 65535 does not fit the uint16 norm index");
+  if (aa.max_norm2 > 65534) raise(Errc::unsupported, "||h||^2 above 65535 does not fit the uint16 norm index");
   if (prob.initial.empty()) raise(Errc::invalid_argument, "problem needs at least one initial condition");
   if (!(prob.eps > 0)) raise(Errc::invalid_argument, "eps must be > 0");
   if ((int)prob.potential.a.size() != s.dim || (int)prob.potential.b.size() != std::max(0, s.dim - 1))
@@ -630,6 +710,7 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
   s.device = opt.device;
   LD_CK(cudaSetDevice(s.device));
   LD_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+  LD_CK(cudaDeviceGetAttribute(&s.num_sms, cudaDevAttrMultiProcessorCount, s.device));
   s.choose_geometry();
 
   // L2-resident ensemble groups: work buffers of the group + shared tables
@@ -843,7 +924,7 @@ SolverInfo Solver::info() const {
   i.M1 = s.M1;
   i.M2 = s.M2;
   i.rank = s.rank;
-  i.method = s.method;
+  i.method = s.method + (s.rank == 1 ? (s.pfa ? "/good-thomas" : "/four-step") : "");
   i.group = s.group;
   const double M = (double)s.M, N = (double)s.N, B = (double)s.batch;
   if (s.rank == 2) {
@@ -853,7 +934,9 @@ SolverInfo Solver::info() const {
     i.launches_per_step = 2;
   } else if (s.method == "circulant") {
     const double G = (double)s.group, groups = std::ceil(B / G);
-    i.bytes_per_pass_col = B * (32.0 * M + 16.0 * N);  // state R+W + V (valid part)
+    // state R+W + V: four-step reads the N valid V entries, Good-Thomas the
+    // position-ordered V_perm (M entries, mask folded in)
+    i.bytes_per_pass_col = B * (32.0 * M + 16.0 * (s.pfa ? M : N));
     i.bytes_per_pass_row = B * 32.0 * M + groups * 16.0 * M;  // state R+W + K^ once per group
     i.bytes_per_step = i.bytes_per_pass_col + i.bytes_per_pass_row;
     i.launches_per_step = 2 * (int)groups;

@@ -420,7 +420,7 @@ int lattdse_solver_info_get(lattdse_solver* s, lattdse_solver_info* out) {
     out->M2 = i.M2;
     out->group = i.group;
     out->rank = i.rank;
-    out->method = i.method == "bluestein" ? 1 : (i.method == "grid" ? 2 : 0);
+    out->method = i.method.rfind("bluestein", 0) == 0 ? 1 : (i.method == "grid" ? 2 : 0);
     out->bytes_per_step = i.bytes_per_step;
     out->bytes_per_pass_col = i.bytes_per_pass_col;
     out->bytes_per_pass_row = i.bytes_per_pass_row;
