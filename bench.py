@@ -115,10 +115,14 @@ def dist_setup(n_gpus):
     return 1, 0, 0, None, None
 
 
+def _dev(dist):
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+
 def max_over_ranks(x, dist, torch):
     if dist is None:
         return x
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_dev(dist))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -126,7 +130,7 @@ def max_over_ranks(x, dist, torch):
 def sum_over_ranks(x, dist, torch):
     if dist is None:
         return x
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_dev(dist))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -189,7 +193,9 @@ def config_dict(cfg, args, note=None):
          "lattice": "CBC prime-n generating vector (paper_1808_06357_b200/catalog.json)" if cfg.rank == 1
          else "product rank-2 lattice (configs.py)",
          "method": args.method, "l2": "flushed (512 MiB memset) before every timed bench step",
-         "parallelism": "replicas only (C1 does not shard)" if args.gpus > 1 else "1 GPU"}
+         "parallelism": ("1 GPU" if args.gpus == 1 else
+                         ("ensemble sharded by member (shard_members), no data-path collective" if cfg.batch > 1
+                          else "replicas only (a single wave function of this size does not shard)"))}
     if note:
         d["note"] = note
     return d
@@ -202,8 +208,16 @@ def run_ours(args, cfg):
     from paper_1808_06357_b200 import configs
 
     lat = configs.lattice(cfg)
-    batch = cfg.batch if args.batch is None else args.batch
-    a, b, c, p = configs.problem(cfg, batch=batch)
+    batch_total = cfg.batch if args.batch is None else args.batch
+    a, b, c, p = configs.problem(cfg, batch=batch_total)
+    if batch_total > 1:
+        # ensemble: shard members across ranks, no data-path collective
+        m0, batch = configs.shard_members(batch_total, rank, world)
+        c, p = c[m0:m0 + batch], p[m0:m0 + batch]
+        members_all = batch_total
+    else:
+        batch = 1  # single wave function: every rank runs a replica
+        members_all = world
     norm2, _, _ = L.aaset_build(lat, with_vectors=False)
     S = L.Solver(lat, cfg.eps, a, b, c, p, cfg.sigma, method=args.method, device=local, norm2=norm2)
     S.set_dt(cfg.dt)
@@ -229,7 +243,7 @@ def run_ours(args, cfg):
     clk = clocks.stop()
     barrier(dist)
     total_ms = max_over_ranks(sum(per_step), dist, torch)
-    work = float(cfg.N) * batch * m * args.steps * world
+    work = float(cfg.N) * members_all * m * args.steps
     value = work / (total_ms * 1e-3)
 
     # ---- per-pass durations (instrumented run, outside the timed region)
@@ -281,7 +295,7 @@ def run_ours(args, cfg):
             S.get_state_ptr(host_out.data_ptr(), batch)
             e2e_times.append(time.perf_counter() - t0)
         e2e_s = max_over_ranks(sum(e2e_times), dist, torch)
-        e2e = {"value": float(cfg.N) * batch * m * args.steps * world / e2e_s, "unit": UNIT,
+        e2e = {"value": float(cfg.N) * members_all * m * args.steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
                "ms_per_step": 1e3 * e2e_s / args.steps}
 
@@ -300,7 +314,7 @@ def run_ours(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (complex fp64)",
+            "scaling": "strong" if batch_total > 1 else "weak", "vs_baseline": None, "dtype": "c128 (complex fp64)",
             "data": "synthetic (seeded BASELINE families, DESIGN.md Seeds)",
             "config": config_dict(cfg, args), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk,

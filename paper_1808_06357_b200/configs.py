@@ -116,3 +116,11 @@ def rank2_product(n1: int, n2: int, d: int):
     c1 = [int(x) for x in z[:h]] + [0] * (d - h)
     c2 = [0] * h + [int(x) % n2 for x in z[h:]]
     return Lattice.create(d, 2, [c1, c2], [n1, n2])
+
+
+def shard_members(batch: int, rank: int, world: int):
+    """Contiguous ensemble shard of `rank` (config 3 batch sharding, SURVEY.md
+    §8(e)): returns (first member, count); shards differ in size by <= 1."""
+    base, extra = divmod(batch, world)
+    m0 = rank * base + min(rank, extra)
+    return m0, base + (1 if rank < extra else 0)
