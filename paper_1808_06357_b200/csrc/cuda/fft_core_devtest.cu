@@ -26,8 +26,8 @@ static double2 root(long long t, long long n) {
   return make_double2((double)cosl(a), (double)sinl(a));
 }
 
-template <int AXIS, int L, int B, int NT, int PROG, int SIGN>
-int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin = -1) {
+template <int AXIS, int L, int B, int NT, int PROG, int SIGN, int MINB = 1>
+int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin = -1, bool timing = false) {
   const long long M = nrows * ncols;
   std::mt19937_64 rng(7);
   std::uniform_real_distribution<double> u(-1, 1);
@@ -62,11 +62,27 @@ int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin
   a.diag_kind = DG_CPLX; a.diag = dd;
   a.pre_tw = pre_tw; a.post_tw = post_tw; a.tw_shift = shift; a.tw_lo = dlo; a.tw_hi = dhi; a.fft_tw = dtw;
   const int smem = SmemGeom<L, B>::bytes;
-  auto fn = fft_pass_kernel<AXIS, L, B, NT, PROG, SIGN>;
+  auto fn = fft_pass_kernel<AXIS, L, B, NT, PROG, SIGN, MINB>;
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   fn<<<dim3((unsigned)((nlines + B - 1) / B), 1), NT, smem>>>(a);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
+  if (timing) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int reps = 50;
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) fn<<<dim3((unsigned)((nlines + B - 1) / B), 1), NT, smem>>>(a);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    std::printf("TIME axis=%d L=%d B=%d NT=%d prog=%d minb=%d ablate=%d: %.2f us/launch\n", AXIS, L, B, NT, PROG, MINB,
+                LATTDSE_ABLATE, 1e3 * ms / reps);
+    cudaFree(din); cudaFree(dx); cudaFree(dd); cudaFree(dtw); cudaFree(dlo); cudaFree(dhi);
+    return 0;
+  }
   std::vector<double2> got(M);
   CK(cudaMemcpy(got.data(), dx, M * 16, cudaMemcpyDeviceToHost));
   // host emulation on host copies
@@ -91,6 +107,13 @@ int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin
 
 int main(int argc, char** argv) {
   int bad = 0;
+  if (argc > 1 && std::string(argv[1]) == "time") {
+    run<AX_ROW, 1728, 1, 192, PROG_DOUBLE, -1, 3>(1215, 1728, 0, 0, -1, true);
+    run<AX_COL, 1215, 2, 288, PROG_DOUBLE, 1, 3>(1215, 1728, 1, 1, -1, true);
+    run<AX_ROW, 720, 1, 256, PROG_DOUBLE, -1, 3>(729, 720, 0, 0, -1, true);
+    run<AX_COL, 729, 2, 192, PROG_DOUBLE, 1, 3>(729, 720, 1, 1, -1, true);
+    return 0;
+  }
   if (argc > 1) {
     bad |= run<AX_COL, 1215, 2, 256, PROG_LOADDIAG, -1>(1215, 1728, 1, 0, 1048583);
     std::printf(bad ? "SOME FAILED\n" : "ALL OK\n");

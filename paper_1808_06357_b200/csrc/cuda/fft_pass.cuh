@@ -25,6 +25,10 @@
 
 #include "fft_core.cuh"
 
+#ifndef LATTDSE_ABLATE
+#define LATTDSE_ABLATE 0  // devtest-only timing ablations: 1 mid diag, 2 stage twiddles, 4 stage-0 loads
+#endif
+
 namespace lattdse_dev {
 
 enum : int { AX_ROW = 0, AX_COL = 1 };
@@ -143,6 +147,7 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
   LD_HD double2 mid(int b, int i, double2 v) const {
     long long j = pos(b, i);
     if (!live(b) || j >= a.nvalid_mid) return make_double2(0.0, 0.0);
+    if (LATTDSE_ABLATE & 1) return v;
     if (dgt) return c_mul(v, dgt[b * L + i]);
     return apply_diag(v, j);
   }
@@ -228,7 +233,9 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
       map(q, b, j);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if (SRC == SRC_GLOBAL)
+        if (SRC == SRC_GLOBAL && (LATTDSE_ABLATE & 4))
+          v[t][r] = c.sm[C::slot(b, j + r * T)];
+        else if (SRC == SRC_GLOBAL)
           v[t][r] = c.gload(b, j + r * T);
         else if (SRC == SRC_TILE)
           v[t][r] = c.tload(b, j + r * T);
@@ -250,8 +257,11 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
         // stage twiddles w^r from table rows r = 1, 4, 16
         const double2* tw = c.a.fft_tw + P::tw_offset(S) + k;
         Pow<R> pw;
-        pw.init(__ldg_d2(tw), R > 4 ? __ldg_d2(tw + 3 * Ns) : make_double2(1.0, 0.0),
-                R > 16 ? __ldg_d2(tw + 15 * Ns) : make_double2(1.0, 0.0));
+        if (LATTDSE_ABLATE & 2)
+          pw.init(make_double2(0.8, 0.6 + k * 1e-9), make_double2(0.6, 0.8), make_double2(0.0, 1.0));
+        else
+          pw.init(__ldg_d2(tw), R > 4 ? __ldg_d2(tw + 3 * Ns) : make_double2(1.0, 0.0),
+                  R > 16 ? __ldg_d2(tw + 15 * Ns) : make_double2(1.0, 0.0));
         sfor<R>([&](auto rc) {
           constexpr int r = decltype(rc)::value;
           if constexpr (r > 0) {

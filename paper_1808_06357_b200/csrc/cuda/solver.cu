@@ -251,6 +251,10 @@ struct Solver::Impl {
   bool use_v2 = std::getenv("LATTDSE_PASS_V2") != nullptr;           // persistent double-buffered passes (opt-in)
   int num_sms = 148;
   int minb_override = std::getenv("LATTDSE_MINB") ? std::atoi(std::getenv("LATTDSE_MINB")) : 0;
+  long long persist_bytes = 0;   // L2 persisting carve-out granted (0: off)
+  // which pass's table is pinned: 1 ROW (K^ / B^), 2 COL (V), 3 both
+  int persist_mode = std::getenv("LATTDSE_L2_PERSIST") ? std::atoi(std::getenv("LATTDSE_L2_PERSIST")) : 1;
+  size_t persist_window = 0;     // max access-policy window
 
   explicit Impl(const Lattice& l) : lat(l) {}
 
@@ -288,7 +292,30 @@ struct Solver::Impl {
       grid = dim3((unsigned)((nlines + k->B - 1) / k->B), (unsigned)nbatch);
     }
     void* args[] = {&a};
-    LD_CK(cudaLaunchKernel(fn, grid, dim3(k->NT), args, (size_t)smem, stream));
+    const bool persist_this = persist_bytes > 0 && prog == PROG_DOUBLE && a.diag_kind == DG_CPLX &&
+                              ((axis == AX_ROW && (persist_mode & 1)) || (axis == AX_COL && (persist_mode & 2)));
+    if (persist_this) {
+      // keep the per-step diagonal table (K^ / V) L2-resident across steps:
+      // it is read once per step and would otherwise be evicted by the
+      // streaming work buffer (profiles/README.md, steady-state DRAM bytes)
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(k->NT);
+      cfg.dynamicSmemBytes = (size_t)smem;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      attr[0].val.accessPolicyWindow.base_ptr = (void*)a.diag;
+      attr[0].val.accessPolicyWindow.num_bytes = std::min<size_t>(persist_window, (size_t)table_bytes(a));
+      attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      LD_CK(cudaLaunchKernelExC(&cfg, fn, args));
+    } else {
+      LD_CK(cudaLaunchKernel(fn, grid, dim3(k->NT), args, (size_t)smem, stream));
+    }
     ++launches;
     if (sync_check) {
       cudaError_t e = cudaStreamSynchronize(stream);
@@ -297,6 +324,11 @@ struct Solver::Impl {
                                       std::to_string(prog) + " sign=" + std::to_string(sign) + (v2 ? " v2" : " v1") +
                                       ": " + cudaGetErrorString(e));
     }
+  }
+  // bytes of the complex diagonal table a DOUBLE pass reads (position order)
+  long long table_bytes(const PassArgs& a) const {
+    return 16LL * (rank == 1 && a.diag == Khat.p ? M : (rank == 1 && a.diag == B1hat.p) || (rank == 1 && a.diag == B2hat.p) ? M
+                                                                                                                     : (pfa && a.diag == Vperm.p ? M : N));
   }
   int grid1d(long long n) const { return (int)std::min<long long>((n + 255) / 256, 148 * 16); }
   void aux_done(const char* what = "aux") {
@@ -712,6 +744,20 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
   LD_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
   LD_CK(cudaDeviceGetAttribute(&s.num_sms, cudaDevAttrMultiProcessorCount, s.device));
   s.choose_geometry();
+  if (s.persist_mode > 0 && s.rank == 1) {
+    int maxp = 0, maxw = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, s.device);
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, s.device);
+    const long long want = 16LL * ((s.persist_mode & 1) ? s.M : 0) + 16LL * ((s.persist_mode & 2) ? s.M : 0);
+    const long long grant = std::min<long long>(want, maxp);
+    if (grant > 0 && maxw > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)grant) == cudaSuccess) {
+      s.persist_bytes = grant;
+      s.persist_window = (size_t)maxw;
+    }
+    cudaGetLastError();
+    if (std::getenv("LATTDSE_VERBOSE"))
+      std::fprintf(stderr, "lattdse: L2 persisting max %d window %d granted %lld\n", maxp, maxw, s.persist_bytes);
+  }
 
   // L2-resident ensemble groups: work buffers of the group + shared tables
   // within ~70% of L2.
