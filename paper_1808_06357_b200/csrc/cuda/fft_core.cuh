@@ -297,8 +297,9 @@ template <int L> struct Plan {
     return o;
   }
   static constexpr int tw_size = tw_offset(nst);
-  // even first radix -> stride-R stage-0 writes conflict; pad 1 slot per 16
-  static constexpr bool swizzle = (radix(0) % 2 == 0) && L >= 16;
+  // even radix in stage 0 of either direction (PlanX<L, true> starts with the
+  // last radix) -> stride-R stage-0 writes conflict; pad 1 slot per 16
+  static constexpr bool swizzle = (radix(0) % 2 == 0 || radix(nst - 1) % 2 == 0) && L >= 16;
   static constexpr int phys(int i) { return swizzle ? i + (i >> 4) : i; }
   static constexpr bool valid() {
     for (int s = 0; s < nst; ++s) {
@@ -308,6 +309,25 @@ template <int L> struct Plan {
     return L >= 2;
   }
   static_assert(valid(), "transform length must factor into radices <= 32 from kRadixPref");
+};
+
+// The plan in forward (REV = false) or reversed radix order. The second
+// transform of a fused pass uses the reversed order so that its first stage
+// touches exactly the elements the first transform's last stage produced.
+template <int L, bool REV> struct PlanX {
+  using P = Plan<L>;
+  static constexpr int nst = P::nst;
+  static constexpr int radix(int s) { return REV ? P::radix(nst - 1 - s) : P::radix(s); }
+  static constexpr int ns(int s) {
+    int p = 1;
+    for (int i = 0; i < s; ++i) p *= radix(i);
+    return p;
+  }
+  static constexpr int tw_offset(int s) {
+    int o = 0;
+    for (int i = 1; i < s; ++i) o += (radix(i) - 1) * ns(i);
+    return o;
+  }
 };
 
 // Host: per-stage twiddle table for a radix plan (layout of Plan::tw_offset),
@@ -330,9 +350,9 @@ inline int build_stage_twiddles(const int* radix, int nst, double2* out) {
   return o;
 }
 
-template <int L> inline int plan_twiddles(double2* out) {
+template <int L> inline int plan_twiddles(double2* out, bool rev = false) {
   int radix[32];
-  for (int s = 0; s < Plan<L>::nst; ++s) radix[s] = Plan<L>::radix(s);
+  for (int s = 0; s < Plan<L>::nst; ++s) radix[s] = Plan<L>::radix(rev ? Plan<L>::nst - 1 - s : s);
   return build_stage_twiddles(radix, Plan<L>::nst, out);
 }
 

@@ -38,19 +38,22 @@ int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin
   for (auto& v : xin) v = make_double2(u(rng), u(rng));
   std::vector<double2> fft_tw(std::max(1, plan_twiddles<L>(nullptr)));
   plan_twiddles<L>(fft_tw.data());
+  std::vector<double2> fft_tw2(std::max(1, plan_twiddles<L>(nullptr, true)));
+  plan_twiddles<L>(fft_tw2.data(), true);
   int shift = 0;
   while ((1LL << (2 * shift)) < M) ++shift;
   long long nlo = 1LL << shift, nhi = (M + nlo - 1) / nlo;
   std::vector<double2> lo(nlo), hi(nhi);
   for (long long t = 0; t < nlo; ++t) lo[t] = root(t, M);
   for (long long t = 0; t < nhi; ++t) hi[t] = root(t * nlo, M);
-  double2 *dx, *dd, *dtw, *dlo, *dhi, *din;
+  double2 *dx, *dd, *dtw, *dtw2, *dlo, *dhi, *din;
   CK(cudaMalloc(&dx, M * 16)); CK(cudaMalloc(&dd, NI * 16)); CK(cudaMalloc(&din, NI * 16));
-  CK(cudaMemcpy(din, xin.data(), NI * 16, cudaMemcpyHostToDevice)); CK(cudaMalloc(&dtw, fft_tw.size() * 16));
+  CK(cudaMemcpy(din, xin.data(), NI * 16, cudaMemcpyHostToDevice)); CK(cudaMalloc(&dtw, fft_tw.size() * 16)); CK(cudaMalloc(&dtw2, fft_tw2.size() * 16));
   CK(cudaMalloc(&dlo, nlo * 16)); CK(cudaMalloc(&dhi, nhi * 16));
   CK(cudaMemcpy(dx, x.data(), M * 16, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dd, diag.data(), NI * 16, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dtw, fft_tw.data(), fft_tw.size() * 16, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dtw2, fft_tw2.data(), fft_tw2.size() * 16, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dlo, lo.data(), nlo * 16, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dhi, hi.data(), nhi * 16, cudaMemcpyHostToDevice));
   PassArgs a{};
@@ -60,7 +63,7 @@ int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin
   const long long nlines = AXIS == AX_ROW ? nrows : ncols;
   a.nlines = (int)nlines;
   a.diag_kind = DG_CPLX; a.diag = dd;
-  a.pre_tw = pre_tw; a.post_tw = post_tw; a.tw_shift = shift; a.tw_lo = dlo; a.tw_hi = dhi; a.fft_tw = dtw;
+  a.pre_tw = pre_tw; a.post_tw = post_tw; a.tw_shift = shift; a.tw_lo = dlo; a.tw_hi = dhi; a.fft_tw = dtw; a.fft_tw2 = dtw2;
   const int smem = SmemGeom<L, B>::bytes;
   auto fn = fft_pass_kernel<AXIS, L, B, NT, PROG, SIGN, MINB>;
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -88,7 +91,7 @@ int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin
   // host emulation on host copies
   PassArgs h = a;
   std::vector<double2> hx = x;
-  h.in = nin > 0 ? xin.data() : hx.data(); h.out = hx.data(); h.diag = diag.data(); h.fft_tw = fft_tw.data(); h.tw_lo = lo.data(); h.tw_hi = hi.data();
+  h.in = nin > 0 ? xin.data() : hx.data(); h.out = hx.data(); h.diag = diag.data(); h.fft_tw = fft_tw.data(); h.fft_tw2 = fft_tw2.data(); h.tw_lo = lo.data(); h.tw_hi = hi.data();
   std::vector<double2> sm(SmemGeom<L, B>::LS * B);
   for (long long blk = 0; blk < (nlines + B - 1) / B; ++blk) {
     Ctx<AXIS, L, B, PROG> c{sm.data(), h, (int)(blk * B), 0};
@@ -110,6 +113,9 @@ int main(int argc, char** argv) {
   if (argc > 1 && std::string(argv[1]) == "time") {
     run<AX_ROW, 1728, 1, 192, PROG_DOUBLE, -1, 3>(1215, 1728, 0, 0, -1, true);
     run<AX_COL, 1215, 2, 288, PROG_DOUBLE, 1, 3>(1215, 1728, 1, 1, -1, true);
+    run<AX_COL, 1215, 2, 288, PROG_DOUBLE, 1, 3>(1215, 1728, 0, 0, -1, true);   // no four-step twiddles
+    run<AX_COL, 1215, 2, 288, PROG_DOUBLE, 1, 2>(1215, 1728, 1, 1, -1, true);
+    run<AX_ROW, 1728, 1, 192, PROG_DOUBLE, -1, 2>(1215, 1728, 0, 0, -1, true);
     run<AX_ROW, 720, 1, 256, PROG_DOUBLE, -1, 3>(729, 720, 0, 0, -1, true);
     run<AX_COL, 729, 2, 192, PROG_DOUBLE, 1, 3>(729, 720, 1, 1, -1, true);
     return 0;

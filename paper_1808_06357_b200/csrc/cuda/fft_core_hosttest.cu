@@ -75,9 +75,12 @@ struct Tables {
   std::vector<double2> fft_tw;
   std::vector<double2> tw_lo, tw_hi;
   int shift = 0;
+  std::vector<double2> fft_tw2;
   template <int L> void build_plan() {
     fft_tw.resize(std::max(1, plan_twiddles<L>(nullptr)));
     plan_twiddles<L>(fft_tw.data());
+    fft_tw2.resize(std::max(1, plan_twiddles<L>(nullptr, true)));
+    plan_twiddles<L>(fft_tw2.data(), true);
   }
   void build(int L, long long M) {
     shift = 0;
@@ -148,6 +151,7 @@ template <int AXIS, int L, int B, int NT, int SIGN1> void test_double_v2(int oth
   a.pre_tw = pre;
   a.post_tw = post;
   a.fft_tw = tb.fft_tw.data();
+  a.fft_tw2 = tb.fft_tw2.data();
   a.tw_lo = tb.tw_lo.data();
   a.tw_hi = tb.tw_hi.data();
   a.tw_shift = tb.shift;
@@ -209,6 +213,7 @@ template <int AXIS, int L, int B, int NT, int SIGN> void test_lines(int other) {
   a.diag_kind = DG_CPLX;
   a.diag = diag.data();
   a.fft_tw = tb.fft_tw.data();
+  a.fft_tw2 = tb.fft_tw2.data();
   a.tw_lo = tb.tw_lo.data();
   a.tw_hi = tb.tw_hi.data();
   a.tw_shift = tb.shift;
@@ -265,6 +270,7 @@ template <int AXIS, int L, int B, int NT, int SIGN1> void test_double(int other,
   a.diag_idx = idx16.data();
   a.lut = lut.data();
   a.fft_tw = tb.fft_tw.data();
+  a.fft_tw2 = tb.fft_tw2.data();
   a.tw_lo = tb.tw_lo.data();
   a.tw_hi = tb.tw_hi.data();
   a.tw_shift = tb.shift;
@@ -318,6 +324,7 @@ template <int M1, int M2> void test_fourstep(long long nvalid) {
   a.diag = ones.data();
   a.post_tw = 1;
   a.fft_tw = t1.fft_tw.data();
+  a.fft_tw2 = t1.fft_tw2.data();
   a.tw_lo = t1.tw_lo.data();
   a.tw_hi = t1.tw_hi.data();
   a.tw_shift = t1.shift;
@@ -332,6 +339,7 @@ template <int M1, int M2> void test_fourstep(long long nvalid) {
   b.ncols = M2;
   b.nlines = M1;
   b.fft_tw = t2.fft_tw.data();
+  b.fft_tw2 = t2.fft_tw2.data();
   emulate<AX_ROW, M2, 1, 64, PROG_LOADDIAG, -1>(b, M1, 1);
   std::vector<cld> xv(M, cld(0));
   for (long long j = 0; j < nvalid; ++j) xv[j] = cld(x[j].x, x[j].y);
@@ -372,6 +380,7 @@ template <int M1, int M2> void test_pfa(long long nvalid) {
   a.diag_kind = DG_CPLX;
   a.diag = dg.data();
   a.fft_tw = t1.fft_tw.data();
+  a.fft_tw2 = t1.fft_tw2.data();
   a.pfa = 1;
   a.pM1 = M1;
   a.pM2 = M2;
@@ -385,6 +394,7 @@ template <int M1, int M2> void test_pfa(long long nvalid) {
   b.ncols = M2;
   b.nlines = M1;
   b.fft_tw = t2.fft_tw.data();
+  b.fft_tw2 = t2.fft_tw2.data();
   emulate<AX_ROW, M2, 1, 64, PROG_LOADDIAG, -1>(b, M1, 1);
   std::vector<cld> xv(M, cld(0));
   for (long long j = 0; j < nvalid; ++j) xv[j] = cld(x[j].x, x[j].y) * cld(dg[j].x, dg[j].y);
@@ -438,6 +448,7 @@ int main(int argc, char** argv) {
     a.diag_kind = DG_CPLX;
     a.diag = dN.data();
     a.fft_tw = t1.fft_tw.data();
+    a.fft_tw2 = t1.fft_tw2.data();
     a.tw_lo = t1.tw_lo.data();
     a.tw_hi = t1.tw_hi.data();
     a.tw_shift = t1.shift;

@@ -25,6 +25,9 @@
 
 #include "fft_core.cuh"
 
+#ifndef LATTDSE_FUSED_MID
+#define LATTDSE_FUSED_MID 1  // fuse T1's last stage, the diag and T2's first stage (reversed plan)
+#endif
 #ifndef LATTDSE_ABLATE
 #define LATTDSE_ABLATE 0  // devtest-only timing ablations: 1 mid diag, 2 stage twiddles, 4 stage-0 loads
 #endif
@@ -53,6 +56,7 @@ struct PassArgs {
   const double2* tw_lo;
   const double2* tw_hi;
   const double2* fft_tw;                   // per-stage twiddles, Plan<L>::tw_offset layout
+  const double2* fft_tw2;                  // same for the reversed plan (second transform of PROG_DOUBLE)
   int nblk;                                // v2: line blocks per batch member
   int ntiles;                              // v2: nblk * batch
   // Good-Thomas (prime-factor) rank-1 layout: position (n1, n2) of the
@@ -191,8 +195,8 @@ template <int R> struct Pow {
 enum : int { SRC_SMEM = 0, SRC_GLOBAL = 1, SRC_TILE = 2 };
 enum : int { DST_SMEM = 0, DST_SMEM_MID = 1, DST_GLOBAL = 2 };
 
-template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, int DST> struct Stage {
-  using P = Plan<L>;
+template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, int DST, bool REV = false> struct Stage {
+  using P = PlanX<L, REV>;
   static constexpr int R = P::radix(S);
   static constexpr int Ns = P::ns(S);
   static constexpr int T = L / R;
@@ -218,9 +222,15 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
     Pow<R> pw;
     pw.init(c.twid(col * T), R > 4 ? c.twid(col * 4 * T) : make_double2(1.0, 0.0),
             R > 16 ? c.twid(col * 16 * T) : make_double2(1.0, 0.0));
+    // base * w^(4q + m) = (base * w^(4q)) * w^m: one product per element
+    double2 bq[(R + 3) / 4];
+    sfor<(R + 3) / 4>([&](auto qc) {
+      constexpr int q = decltype(qc)::value;
+      bq[q] = q == 0 ? base : c_mul(base, pw.template get<4 * q>());
+    });
     sfor<R>([&](auto rc) {
       constexpr int r = decltype(rc)::value;
-      const double2 w = r == 0 ? base : c_mul(base, pw.template get<r>());
+      const double2 w = (r % 4 == 0) ? bq[r / 4] : c_mul(bq[r / 4], pw.template get<r % 4>());
       v[r] = conj ? c_mulc(v[r], w) : c_mul(v[r], w);
     });
   }
@@ -255,7 +265,7 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
       const int k = j % Ns;
       if (Ns > 1) {
         // stage twiddles w^r from table rows r = 1, 4, 16
-        const double2* tw = c.a.fft_tw + P::tw_offset(S) + k;
+        const double2* tw = (REV ? c.a.fft_tw2 : c.a.fft_tw) + P::tw_offset(S) + k;
         Pow<R> pw;
         if (LATTDSE_ABLATE & 2)
           pw.init(make_double2(0.8, 0.6 + k * 1e-9), make_double2(0.6, 0.8), make_double2(0.0, 1.0));
@@ -288,6 +298,62 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
   }
 };
 
+// Fused middle of PROG_DOUBLE: the first transform's last stage (forward
+// plan, sign SIGN), the diagonal multiply, and the second transform's first
+// stage (reversed plan, sign -SIGN, Ns = 1) on the same registers: with the
+// reversed plan both stages cover elements j + r*T of task j, so the
+// intermediate never goes through shared memory.
+template <int AXIS, int L, int B, int NT, int SIGN, int SRC, int DST> struct MidStage {
+  using P1 = PlanX<L, false>;
+  static constexpr int S1 = P1::nst - 1;
+  static constexpr int R = P1::radix(S1);
+  static constexpr int Ns = P1::ns(S1);
+  static constexpr int T = L / R;
+  static_assert(T == Ns, "last stage covers j + r*T");
+  static constexpr int TASKS = B * T;
+  static constexpr int TPT = (TASKS + NT - 1) / NT;
+  static constexpr int src = SRC, dst = DST, nt = NT;
+  using First = Stage<AXIS, L, B, NT, PROG_DOUBLE, S1, SIGN, SRC, DST_SMEM, false>;
+  using C = Ctx<AXIS, L, B, PROG_DOUBLE>;
+
+  LD_HD static void read(const C& c, int tid, double2 (&v)[TPT][R]) { First::read(c, tid, v); }
+  LD_HD static void write(const C& c, int tid, double2 (&v)[TPT][R]) {
+#pragma unroll
+    for (int t = 0; t < TPT; ++t) {
+      int q = tid + t * NT;
+      if (TASKS % NT != 0 && q >= TASKS) break;
+      int b, j;
+      First::map(q, b, j);
+      if (Ns > 1) {
+        const double2* tw = c.a.fft_tw + P1::tw_offset(S1) + j;
+        Pow<R> pw;
+        pw.init(__ldg_d2(tw), R > 4 ? __ldg_d2(tw + 3 * Ns) : make_double2(1.0, 0.0),
+                R > 16 ? __ldg_d2(tw + 15 * Ns) : make_double2(1.0, 0.0));
+        sfor<R>([&](auto rc) {
+          constexpr int r = decltype(rc)::value;
+          if constexpr (r > 0) {
+            const double2 w = pw.template get<r>();
+            v[t][r] = SIGN < 0 ? c_mul(v[t][r], w) : c_mulc(v[t][r], w);
+          }
+        });
+      }
+      DFT<R, SIGN>::run(v[t]);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[t][r] = c.mid(b, j + r * T, v[t][r]);
+      DFT<R, -SIGN>::run(v[t]);  // second transform, stage 0 (Ns = 1: no twiddle)
+      // stage-0 outputs of the reversed plan: idxD = j*R, positions j*R + r
+      if (DST == DST_GLOBAL && AXIS == AX_COL && c.a.post_tw) First::fourstep(c, b, j, v[t], false);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (DST == DST_GLOBAL)
+          c.gstore(b, j * R + r, v[t][r]);
+        else
+          c.sm[C::slot(b, j * R + r)] = v[t][r];
+      }
+    }
+  }
+};
+
 #if defined(__CUDACC__)
 struct DevExec {
   template <class St, class C> __device__ __forceinline__ static void stage(const C& c) {
@@ -300,25 +366,35 @@ struct DevExec {
 };
 #endif
 
-// Run one transform of sign SIGN over the CTA's lines.
+// Run stages [S0, nst) of one transform of sign SIGN over the CTA's lines.
 #pragma nv_exec_check_disable
-template <class Exec, int AXIS, int L, int B, int NT, int PROG, int SIGN, int FIRST, int LAST, class C>
+template <class Exec, int AXIS, int L, int B, int NT, int PROG, int SIGN, int FIRST, int LAST, bool REV = false,
+          int S0 = 0, int S1 = Plan<L>::nst, class C>
 LD_HD void run_fft(const C& c) {
   constexpr int nst = Plan<L>::nst;
-  sfor<nst>([&](auto sc) {
-    constexpr int s = decltype(sc)::value;
+  sfor<S1 - S0>([&](auto sc) {
+    constexpr int s = decltype(sc)::value + S0;
     constexpr int src = (s == 0) ? FIRST : SRC_SMEM;
     constexpr int dst = (s == nst - 1) ? LAST : DST_SMEM;
-    Exec::template stage<Stage<AXIS, L, B, NT, PROG, s, SIGN, src, dst>>(c);
+    Exec::template stage<Stage<AXIS, L, B, NT, PROG, s, SIGN, src, dst, REV>>(c);
   });
 }
 
 #pragma nv_exec_check_disable
 template <class Exec, int AXIS, int L, int B, int NT, int PROG, int SIGN1, int FIRST = SRC_GLOBAL>
 LD_HD void run_pass(const Ctx<AXIS, L, B, PROG>& c) {
-  if constexpr (PROG == PROG_DOUBLE) {
+  if constexpr (PROG == PROG_DOUBLE && !LATTDSE_FUSED_MID) {
     run_fft<Exec, AXIS, L, B, NT, PROG, SIGN1, FIRST, DST_SMEM_MID>(c);
     run_fft<Exec, AXIS, L, B, NT, PROG, -SIGN1, SRC_SMEM, DST_GLOBAL>(c);
+  } else if constexpr (PROG == PROG_DOUBLE) {
+    constexpr int nst = Plan<L>::nst;
+    // first transform up to (excluding) its last stage
+    run_fft<Exec, AXIS, L, B, NT, PROG, SIGN1, FIRST, DST_SMEM, false, 0, nst - 1>(c);
+    // last stage + diag + first stage of the reversed second transform
+    Exec::template stage<MidStage<AXIS, L, B, NT, SIGN1, (nst == 1 ? FIRST : SRC_SMEM),
+                                  (nst == 1 ? DST_GLOBAL : DST_SMEM)>>(c);
+    // remaining stages of the second transform (reversed plan)
+    run_fft<Exec, AXIS, L, B, NT, PROG, -SIGN1, SRC_SMEM, DST_GLOBAL, true, 1, nst>(c);
   } else {
     run_fft<Exec, AXIS, L, B, NT, PROG, SIGN1, FIRST, DST_GLOBAL>(c);
   }

@@ -1,0 +1,2 @@
+#include "../pass_instantiate.cuh"
+LATTDSE_INSTANTIATE_L(324)

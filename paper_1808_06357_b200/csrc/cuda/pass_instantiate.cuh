@@ -35,7 +35,9 @@ template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
     k.fn_mb[4] = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN, 4>);
     // measured on C1 (profiles/README.md): 3 resident CTAs/SM balance register
     // caps (small L1-resident spills) against occupancy for 5-10 warp CTAs
-    k.default_mb = G::NT <= 320 ? 3 : (G::NT <= 512 ? 2 : 1);
+    // ROW: 3 CTAs/SM; COL (four-step twiddle math in the fused stages) keeps
+    // more registers at 2 CTAs/SM
+    k.default_mb = G::NT > 320 ? 2 : (AXIS == lattdse_dev::AX_ROW ? 3 : 2);
   }
   if constexpr (PROG == lattdse_dev::PROG_DOUBLE && G::smem2 <= 227 * 1024) {
     k.fn2 = reinterpret_cast<const void*>(&lattdse_dev::fft_pass2_kernel<AXIS, L, G::B, G::NT, SIGN>);

@@ -242,7 +242,7 @@ struct Solver::Impl {
   DBuf<double2> V, Vh, Ventry, Vexit, kin_lut, kin_full, Vperm;
   DBuf<unsigned short> nidx_perm;  // Good-Thomas: norm index in position order (sentinel = zero phase)
   DBuf<double2> Khat, B1hat, B2hat, chirp, chirp_c, chirp_n;
-  DBuf<double2> tw_col, tw_row, tw_lo, tw_hi, scal;
+  DBuf<double2> tw_col, tw_row, tw_col2, tw_row2, tw_lo, tw_hi, scal;
   DBuf<double> partial;
   DBuf<char> flush;
   bool bluestein_tables = false;
@@ -346,6 +346,7 @@ struct Solver::Impl {
     a.tw_lo = tw_lo.p;
     a.tw_hi = tw_hi.p;
     a.fft_tw = axis == AX_COL ? tw_col.p : tw_row.p;
+    a.fft_tw2 = axis == AX_COL ? tw_col2.p : tw_row2.p;
     a.ncols = (int)M2;
     a.pfa = pfa ? 1 : 0;
     a.pM1 = (int)M1;
@@ -460,24 +461,59 @@ struct Solver::Impl {
       return;
     }
     const long long need = 2 * N - 1;
-    // best four-step (any factors) and best Good-Thomas (coprime) split
-    long long best = -1, b1 = 0, b2 = 0, bestp = -1, p1 = 0, p2 = 0;
-    double bal = 0, balp = 0;
-    auto better = [](long long m, double bl, int L1, long long cur, double curbal, long long curL1) {
-      return cur < 0 || m < cur || (m == cur && (bl < curbal - 1e-12 || (std::fabs(bl - curbal) <= 1e-12 && L1 < curL1)));
+    if (const char* g = std::getenv("LATTDSE_GEOM")) {  // "M1xM2" override (experiments)
+      long long g1 = 0, g2 = 0;
+      if (std::sscanf(g, "%lldx%lld", &g1, &g2) == 2 && g1 * g2 >= need && dev::find_pass_kernel(AX_COL, (int)g1, PROG_DOUBLE, -1) &&
+          dev::find_pass_kernel(AX_ROW, (int)g2, PROG_DOUBLE, -1)) {
+        M1 = g1;
+        M2 = g2;
+        M = g1 * g2;
+        pfa = std::getenv("LATTDSE_PFA") != nullptr && std::gcd(g1, g2) == 1;
+        return;
+      }
+    }
+    // Among the splits with the smallest M (within 0.5%), take the one with
+    // the lowest measured pass cost (ps per element, C1/C3 sweeps in
+    // profiles/README.md); unmeasured lengths get a neutral estimate.
+    // ps per element per pass; C1 sweep (M = 2099520) where measured, else
+    // the C3 sweep (M = 524880, 8 members) scaled by 1.15 to C1's occupancy
+    auto col_cost = [](int L) {
+      switch (L) {
+        case 486: return 19.4; case 729: return 21.4; case 1296: return 22.7; case 1215: return 22.7;
+        case 972: return 22.5; case 648: return 23.5; case 1458: return 25.4; case 810: return 25.5;
+        case 432: return 26.1; case 1944: return 26.4; case 1620: return 26.6; case 1728: return 27.5;
+        case 1080: return 27.6; case 540: return 31.4; case 405: return 33.9; case 720: return 37.3;
+        case 1440: return 38.8; default: return 30.0;
+      }
     };
+    auto row_cost = [](int L) {
+      switch (L) {
+        case 486: return 14.8; case 729: return 15.3; case 972: return 15.3; case 1620: return 16.7;
+        case 1296: return 18.0; case 648: return 18.2; case 1728: return 18.2; case 1215: return 18.8;
+        case 2160: return 18.8; case 1080: return 19.6; case 540: return 21.5; case 810: return 22.0;
+        case 720: return 22.1; case 1440: return 20.8; case 1458: return 22.7; case 1944: return 23.6;
+        case 405: return 24.8; case 432: return 25.0; default: return 22.0;
+      }
+    };
+    long long mmin = -1;
     for (int L1 : dev::pass_lengths(AX_COL))
       for (int L2 : dev::pass_lengths(AX_ROW)) {
-        long long m = (long long)L1 * L2;
-        if (m < need) continue;
-        double bl = std::fabs(std::log((double)L1 / L2));
-        if (better(m, bl, L1, best, bal, b1)) { best = m; b1 = L1; b2 = L2; bal = bl; }
-        if (std::gcd(L1, L2) == 1 && better(m, bl, L1, bestp, balp, p1)) { bestp = m; p1 = L1; p2 = L2; balp = bl; }
+        const long long m = (long long)L1 * L2;
+        if (m >= need && (mmin < 0 || m < mmin)) mmin = m;
       }
-    if (best < 0) raise(Errc::unsupported, "N=" + std::to_string(N) + " exceeds the single-level four-step range");
-    // Good-Thomas needs no four-step twiddles (opt-in until it beats the four-step path)
+    if (mmin < 0) raise(Errc::unsupported, "N=" + std::to_string(N) + " exceeds the single-level four-step range");
+    long long best = -1, b1 = 0, b2 = 0, bestp = -1, p1 = 0, p2 = 0;
+    double bcost = 0, pcost = 0;
+    for (int L1 : dev::pass_lengths(AX_COL))
+      for (int L2 : dev::pass_lengths(AX_ROW)) {
+        const long long m = (long long)L1 * L2;
+        if (m < need || (double)m > 1.005 * (double)mmin) continue;
+        const double cost = (double)m * (col_cost(L1) + row_cost(L2));
+        if (best < 0 || cost < bcost) { best = m; b1 = L1; b2 = L2; bcost = cost; }
+        if (std::gcd(L1, L2) == 1 && (bestp < 0 || cost < pcost)) { bestp = m; p1 = L1; p2 = L2; pcost = cost; }
+      }
     const bool allow_pfa = std::getenv("LATTDSE_PFA") != nullptr;  // opt-in: see DESIGN.md
-    if (allow_pfa && bestp > 0 && (double)bestp <= 1.03 * (double)best) {
+    if (allow_pfa && bestp > 0) {
       pfa = true;
       M = bestp;
       M1 = p1;
@@ -495,16 +531,20 @@ struct Solver::Impl {
       b.alloc(h.size());
       LD_CK(cudaMemcpyAsync(b.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
     };
-    auto stage_tw = [&](int axis, long long L) {
+    auto stage_tw = [&](int axis, long long L, bool rev) {
       const dev::PassKernel* k = dev::find_pass_kernel(axis, (int)L, PROG_DOUBLE, -1);
       if (!k) raise(Errc::unsupported, "no pass kernel for L=" + std::to_string(L));
-      const int n = std::max(1, build_stage_twiddles(k->radix, k->nst, nullptr));
+      int radix[16];
+      for (int s = 0; s < k->nst; ++s) radix[s] = k->radix[rev ? k->nst - 1 - s : s];
+      const int n = std::max(1, build_stage_twiddles(radix, k->nst, nullptr));
       std::vector<double2> t(n, make_double2(1.0, 0.0));
-      build_stage_twiddles(k->radix, k->nst, t.data());
+      build_stage_twiddles(radix, k->nst, t.data());
       return t;
     };
-    up(tw_col, stage_tw(AX_COL, M1));
-    up(tw_row, stage_tw(AX_ROW, M2));
+    up(tw_col, stage_tw(AX_COL, M1, false));
+    up(tw_row, stage_tw(AX_ROW, M2, false));
+    up(tw_col2, stage_tw(AX_COL, M1, true));
+    up(tw_row2, stage_tw(AX_ROW, M2, true));
     tw_shift = 0;
     while ((1LL << (2 * tw_shift)) < M) ++tw_shift;
     const long long nlo = 1LL << tw_shift, nhi = (M + nlo - 1) / nlo;
@@ -750,6 +790,7 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
     cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, s.device);
     const long long want = 16LL * ((s.persist_mode & 1) ? s.M : 0) + 16LL * ((s.persist_mode & 2) ? s.M : 0);
     const long long grant = std::min<long long>(want, maxp);
+    cudaCtxResetPersistingL2Cache();  // drop persisting lines left by earlier work on this device
     if (grant > 0 && maxw > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)grant) == cudaSuccess) {
       s.persist_bytes = grant;
       s.persist_window = (size_t)maxw;
@@ -791,6 +832,7 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
 Solver::~Solver() {
   if (p_ && p_->stream) {
     cudaStreamSynchronize(p_->stream);
+    if (p_->persist_bytes > 0) cudaCtxResetPersistingL2Cache();
     cudaStreamDestroy(p_->stream);
   }
 }
