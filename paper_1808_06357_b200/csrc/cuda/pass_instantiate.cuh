@@ -4,6 +4,10 @@
 #include "fft_pass.cuh"
 #include "pass_registry.hpp"
 
+#ifndef LATTDSE_COL_B1_MIN
+#define LATTDSE_COL_B1_MIN 4096  // columns this long: one column per CTA (smem for 3 CTAs/SM)
+#endif
+
 namespace lattdse::dev {
 
 // Launch geometry per (axis, L):
@@ -13,7 +17,7 @@ namespace lattdse::dev {
 // NT covers the busiest stage (B * L / R_min tasks) so no thread loops.
 template <int AXIS, int L> struct Geometry {
   static constexpr int B = AXIS == lattdse_dev::AX_ROW ? (L >= 256 ? 1 : 256 / L)
-                                                       : (L >= 512 ? 2 : (L >= 128 ? 4 : 8));
+                                                       : (L >= LATTDSE_COL_B1_MIN ? 1 : (L >= 512 ? 2 : (L >= 128 ? 4 : 8)));
   static constexpr int raw = B * lattdse_dev::Plan<L>::max_tasks();
   static constexpr int NT = raw <= 32 ? 32 : (raw >= 512 ? 512 : ((raw + 31) / 32) * 32);
   static constexpr int smem2 = 2 * lattdse_dev::SmemGeom<L, B>::bytes + 2 * B * L * 16;

@@ -251,6 +251,14 @@ struct Solver::Impl {
   bool use_v2 = std::getenv("LATTDSE_PASS_V2") != nullptr;           // persistent double-buffered passes (opt-in)
   int num_sms = 148;
   int minb_override = std::getenv("LATTDSE_MINB") ? std::atoi(std::getenv("LATTDSE_MINB")) : 0;
+  // CUDA graphs of kGraphSteps identical middle steps, per (group start, size)
+  static constexpr int kGraphSteps = 32;
+  std::map<std::pair<long long, long long>, cudaGraphExec_t> graphs;
+  bool use_graphs = std::getenv("LATTDSE_NO_GRAPHS") == nullptr;
+  void drop_graphs() {
+    for (auto& [k, g] : graphs) cudaGraphExecDestroy(g);
+    graphs.clear();
+  }
   long long persist_bytes = 0;   // L2 persisting carve-out granted (0: off)
   // which pass's table is pinned: 1 ROW (K^ / B^), 2 COL (V), 3 both
   int persist_mode = std::getenv("LATTDSE_L2_PERSIST") ? std::atoi(std::getenv("LATTDSE_L2_PERSIST")) : 1;
@@ -615,6 +623,7 @@ struct Solver::Impl {
   }
 
   void build_propagator(double dt) {
+    drop_graphs();
     // potential phases: V = exp(-i dt v / eps), Vh = exp(-i dt v / (2 eps))
     V.alloc(N);
     Vh.alloc(N);
@@ -713,7 +722,33 @@ struct Solver::Impl {
         }
       } else if (method == "circulant") {
         timed(pt, true, [&] { r1_col_entry(s, N, Vh.p, w, gb); });
-        for (long long k = 0; k < nsteps; ++k) {
+        long long k = 0;
+        // middle steps (ROW, COL) in graph chunks: identical launches, so the
+        // GPU runs them back to back without host launch latency
+        if (!pt && use_graphs && !sync_check) {
+          const long long chunks = (nsteps - 1) / kGraphSteps;
+          if (chunks > 0) {
+            cudaGraphExec_t& ge = graphs[{g0, gb}];
+            if (!ge) {
+              cudaGraph_t g;
+              LD_CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+              for (int i = 0; i < kGraphSteps; ++i) {
+                r1_row_mid(w, Khat.p, gb);
+                r1_col_mid(w, V.p, gb);
+              }
+              LD_CK(cudaStreamEndCapture(stream, &g));
+              LD_CK(cudaGraphInstantiate(&ge, g, 0));
+              cudaGraphDestroy(g);
+              launches -= 2 * kGraphSteps;  // counted per replay below
+            }
+            for (long long c = 0; c < chunks; ++c) {
+              LD_CK(cudaGraphLaunch(ge, stream));
+              launches += 2 * kGraphSteps;
+            }
+            k = chunks * kGraphSteps;
+          }
+        }
+        for (; k < nsteps; ++k) {
           timed(pt, false, [&] { r1_row_mid(w, Khat.p, gb); });
           if (k + 1 < nsteps)
             timed(pt, true, [&] { r1_col_mid(w, V.p, gb); });
@@ -832,6 +867,7 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
 Solver::~Solver() {
   if (p_ && p_->stream) {
     cudaStreamSynchronize(p_->stream);
+    p_->drop_graphs();
     if (p_->persist_bytes > 0) cudaCtxResetPersistingL2Cache();
     cudaStreamDestroy(p_->stream);
   }
