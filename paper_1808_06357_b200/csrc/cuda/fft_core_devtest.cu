@@ -92,7 +92,7 @@ int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin
   PassArgs h = a;
   std::vector<double2> hx = x;
   h.in = nin > 0 ? xin.data() : hx.data(); h.out = hx.data(); h.diag = diag.data(); h.fft_tw = fft_tw.data(); h.fft_tw2 = fft_tw2.data(); h.tw_lo = lo.data(); h.tw_hi = hi.data();
-  std::vector<double2> sm(SmemGeom<L, B>::LS * B);
+  std::vector<double2> sm(SmemGeom<L, B>::bytes / 16);
   for (long long blk = 0; blk < (nlines + B - 1) / B; ++blk) {
     Ctx<AXIS, L, B, PROG> c{sm.data(), h, (int)(blk * B), 0};
     run_pass<HostExec, AXIS, L, B, NT, PROG, SIGN>(c);

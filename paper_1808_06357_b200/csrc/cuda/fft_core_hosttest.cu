@@ -95,7 +95,7 @@ struct Tables {
 
 template <int AXIS, int L, int B, int NT, int PROG, int SIGN1>
 void emulate(PassArgs a, int nlines, int nbatch) {
-  std::vector<double2> sm(SmemGeom<L, B>::LS * B);
+  std::vector<double2> sm(SmemGeom<L, B>::bytes / 16);
   for (int bat = 0; bat < nbatch; ++bat)
     for (int blk = 0; blk < (nlines + B - 1) / B; ++blk) {
       Ctx<AXIS, L, B, PROG> c{sm.data(), a, blk * B, bat};
@@ -107,7 +107,7 @@ void emulate(PassArgs a, int nlines, int nbatch) {
 template <int AXIS, int L, int B, int NT, int SIGN1>
 void emulate_v2(PassArgs a, int nlines, int nbatch) {
   using C = Ctx<AXIS, L, B, PROG_DOUBLE>;
-  std::vector<double2> sm(SmemGeom<L, B>::LS * B), dg(B * L);
+  std::vector<double2> sm(SmemGeom<L, B>::bytes / 16), dg(B * L);
   const int nblk = (nlines + B - 1) / B;
   for (int t = 0; t < nblk * nbatch; ++t) {
     const int line0 = (t % nblk) * B;

@@ -28,6 +28,9 @@
 #ifndef LATTDSE_FUSED_MID
 #define LATTDSE_FUSED_MID 1  // fuse T1's last stage, the diag and T2's first stage (reversed plan)
 #endif
+#ifndef LATTDSE_PINGPONG
+#define LATTDSE_PINGPONG 1  // two shared buffers: stage s reads one, writes the other (1 barrier/stage)
+#endif
 #ifndef LATTDSE_ABLATE
 #define LATTDSE_ABLATE 0  // devtest-only timing ablations: 1 mid diag, 2 stage twiddles, 4 stage-0 loads
 #endif
@@ -76,11 +79,14 @@ template <int L, int B> struct SmemGeom {
     return ((want - span % 8) % 8 + 8) % 8;
   }
   static constexpr int LS = span + pad();
-  static constexpr int bytes = B * LS * 16;
+  static constexpr int tile = B * LS;  // slots of one buffer
+  // ping-pong only while two buffers still leave room for 2+ CTAs per SM
+  static constexpr bool pp = LATTDSE_PINGPONG && tile * 16 <= 48 * 1024;
+  static constexpr int bytes = (pp ? 2 : 1) * tile * 16;
 };
 
 template <int AXIS, int L, int B, int PROG> struct Ctx {
-  double2* sm;
+  double2* sm;   // buffer 0 (buffer 1 follows at sm + SmemGeom::tile when ping-ponging)
   PassArgs a;  // by value: fields resolve to parameter-bank operands, not pointer loads
   int line0;
   long long bat;
@@ -88,6 +94,8 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
 
   static constexpr int LS = SmemGeom<L, B>::LS;
   LD_HD static int slot(int b, int i) { return b * LS + Plan<L>::phys(i); }
+  // buffer used as the source of stage-sequence position p (0, 1, 2, ...)
+  LD_HD double2* buf(int p) const { return (SmemGeom<L, B>::pp && (p & 1)) ? sm + SmemGeom<L, B>::tile : sm; }
 
   // array position of element (b, i) in the 2-D view
   LD_HD long long pos(int b, int i) const {
@@ -133,7 +141,7 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
   }
   // v2 stage-0 source: the prefetched tile (masked entries were zero-filled)
   LD_HD double2 tload(int b, int i) const {
-    double2 v = sm[slot(b, i)];
+    double2 v = sm[slot(b, i)];  // the tile was loaded into buf(0)
     if (PROG == PROG_LOADDIAG) {
       long long j = in_index(b, i);
       if (live(b) && j < a.nvalid_in) v = apply_diag(v, j);
@@ -195,7 +203,10 @@ template <int R> struct Pow {
 enum : int { SRC_SMEM = 0, SRC_GLOBAL = 1, SRC_TILE = 2 };
 enum : int { DST_SMEM = 0, DST_SMEM_MID = 1, DST_GLOBAL = 2 };
 
-template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, int DST, bool REV = false> struct Stage {
+// Stage S of a transform, at position Q of the pass's stage sequence: reads
+// shared buffer buf(Q), writes buf(Q+1) (the same buffer unless ping-ponging).
+template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, int DST, bool REV = false, int Q = S>
+struct Stage {
   using P = PlanX<L, REV>;
   static constexpr int R = P::radix(S);
   static constexpr int Ns = P::ns(S);
@@ -203,6 +214,7 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
   static constexpr int TASKS = B * T;
   static constexpr int TPT = (TASKS + NT - 1) / NT;
   static constexpr int src = SRC, dst = DST, nt = NT;
+  static constexpr bool pp = SmemGeom<L, B>::pp;
   using C = Ctx<AXIS, L, B, PROG>;
 
   LD_HD static void map(int q, int& b, int& j) {
@@ -244,13 +256,13 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (SRC == SRC_GLOBAL && (LATTDSE_ABLATE & 4))
-          v[t][r] = c.sm[C::slot(b, j + r * T)];
+          v[t][r] = c.buf(Q)[C::slot(b, j + r * T)];
         else if (SRC == SRC_GLOBAL)
           v[t][r] = c.gload(b, j + r * T);
         else if (SRC == SRC_TILE)
           v[t][r] = c.tload(b, j + r * T);
         else
-          v[t][r] = c.sm[C::slot(b, j + r * T)];
+          v[t][r] = c.buf(Q)[C::slot(b, j + r * T)];
       }
       if (SRC != SRC_SMEM && AXIS == AX_COL && c.a.pre_tw) fourstep(c, b, j, v[t], true);
     }
@@ -290,9 +302,9 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
         if (DST == DST_GLOBAL)
           c.gstore(b, pos, v[t][r]);
         else if (DST == DST_SMEM_MID)
-          c.sm[C::slot(b, pos)] = c.mid(b, pos, v[t][r]);
+          c.buf(Q + 1)[C::slot(b, pos)] = c.mid(b, pos, v[t][r]);
         else
-          c.sm[C::slot(b, pos)] = v[t][r];
+          c.buf(Q + 1)[C::slot(b, pos)] = v[t][r];
       }
     }
   }
@@ -303,7 +315,7 @@ template <int AXIS, int L, int B, int NT, int PROG, int S, int SIGN, int SRC, in
 // stage (reversed plan, sign -SIGN, Ns = 1) on the same registers: with the
 // reversed plan both stages cover elements j + r*T of task j, so the
 // intermediate never goes through shared memory.
-template <int AXIS, int L, int B, int NT, int SIGN, int SRC, int DST> struct MidStage {
+template <int AXIS, int L, int B, int NT, int SIGN, int SRC, int DST, int Q> struct MidStage {
   using P1 = PlanX<L, false>;
   static constexpr int S1 = P1::nst - 1;
   static constexpr int R = P1::radix(S1);
@@ -313,7 +325,8 @@ template <int AXIS, int L, int B, int NT, int SIGN, int SRC, int DST> struct Mid
   static constexpr int TASKS = B * T;
   static constexpr int TPT = (TASKS + NT - 1) / NT;
   static constexpr int src = SRC, dst = DST, nt = NT;
-  using First = Stage<AXIS, L, B, NT, PROG_DOUBLE, S1, SIGN, SRC, DST_SMEM, false>;
+  static constexpr bool pp = SmemGeom<L, B>::pp;
+  using First = Stage<AXIS, L, B, NT, PROG_DOUBLE, S1, SIGN, SRC, DST_SMEM, false, Q>;
   using C = Ctx<AXIS, L, B, PROG_DOUBLE>;
 
   LD_HD static void read(const C& c, int tid, double2 (&v)[TPT][R]) { First::read(c, tid, v); }
@@ -348,7 +361,7 @@ template <int AXIS, int L, int B, int NT, int SIGN, int SRC, int DST> struct Mid
         if (DST == DST_GLOBAL)
           c.gstore(b, j * R + r, v[t][r]);
         else
-          c.sm[C::slot(b, j * R + r)] = v[t][r];
+          c.buf(Q + 1)[C::slot(b, j * R + r)] = v[t][r];
       }
     }
   }
@@ -359,7 +372,7 @@ struct DevExec {
   template <class St, class C> __device__ __forceinline__ static void stage(const C& c) {
     double2 v[St::TPT][St::R];
     St::read(c, threadIdx.x, v);
-    if (St::src != SRC_GLOBAL) __syncthreads();  // in place: all reads before any write
+    if (!St::pp && St::src != SRC_GLOBAL) __syncthreads();  // in place: all reads before any write
     St::write(c, threadIdx.x, v);
     if (St::dst != DST_GLOBAL) __syncthreads();
   }
@@ -369,14 +382,14 @@ struct DevExec {
 // Run stages [S0, nst) of one transform of sign SIGN over the CTA's lines.
 #pragma nv_exec_check_disable
 template <class Exec, int AXIS, int L, int B, int NT, int PROG, int SIGN, int FIRST, int LAST, bool REV = false,
-          int S0 = 0, int S1 = Plan<L>::nst, class C>
+          int S0 = 0, int S1 = Plan<L>::nst, int QB = 0, class C>
 LD_HD void run_fft(const C& c) {
   constexpr int nst = Plan<L>::nst;
   sfor<S1 - S0>([&](auto sc) {
     constexpr int s = decltype(sc)::value + S0;
     constexpr int src = (s == 0) ? FIRST : SRC_SMEM;
     constexpr int dst = (s == nst - 1) ? LAST : DST_SMEM;
-    Exec::template stage<Stage<AXIS, L, B, NT, PROG, s, SIGN, src, dst, REV>>(c);
+    Exec::template stage<Stage<AXIS, L, B, NT, PROG, s, SIGN, src, dst, REV, QB + s - S0>>(c);
   });
 }
 
@@ -384,17 +397,18 @@ LD_HD void run_fft(const C& c) {
 template <class Exec, int AXIS, int L, int B, int NT, int PROG, int SIGN1, int FIRST = SRC_GLOBAL>
 LD_HD void run_pass(const Ctx<AXIS, L, B, PROG>& c) {
   if constexpr (PROG == PROG_DOUBLE && !LATTDSE_FUSED_MID) {
+    constexpr int nst = Plan<L>::nst;
     run_fft<Exec, AXIS, L, B, NT, PROG, SIGN1, FIRST, DST_SMEM_MID>(c);
-    run_fft<Exec, AXIS, L, B, NT, PROG, -SIGN1, SRC_SMEM, DST_GLOBAL>(c);
+    run_fft<Exec, AXIS, L, B, NT, PROG, -SIGN1, SRC_SMEM, DST_GLOBAL, false, 0, nst, nst>(c);
   } else if constexpr (PROG == PROG_DOUBLE) {
     constexpr int nst = Plan<L>::nst;
     // first transform up to (excluding) its last stage
-    run_fft<Exec, AXIS, L, B, NT, PROG, SIGN1, FIRST, DST_SMEM, false, 0, nst - 1>(c);
+    run_fft<Exec, AXIS, L, B, NT, PROG, SIGN1, FIRST, DST_SMEM, false, 0, nst - 1, 0>(c);
     // last stage + diag + first stage of the reversed second transform
     Exec::template stage<MidStage<AXIS, L, B, NT, SIGN1, (nst == 1 ? FIRST : SRC_SMEM),
-                                  (nst == 1 ? DST_GLOBAL : DST_SMEM)>>(c);
+                                  (nst == 1 ? DST_GLOBAL : DST_SMEM), nst - 1>>(c);
     // remaining stages of the second transform (reversed plan)
-    run_fft<Exec, AXIS, L, B, NT, PROG, -SIGN1, SRC_SMEM, DST_GLOBAL, true, 1, nst>(c);
+    run_fft<Exec, AXIS, L, B, NT, PROG, -SIGN1, SRC_SMEM, DST_GLOBAL, true, 1, nst, nst>(c);
   } else {
     run_fft<Exec, AXIS, L, B, NT, PROG, SIGN1, FIRST, DST_GLOBAL>(c);
   }
@@ -456,7 +470,7 @@ __global__ void __launch_bounds__(NT, MINB) fft_pass_kernel(const __grid_constan
 template <int AXIS, int L, int B, int NT, int SIGN1>
 __global__ void __launch_bounds__(NT) fft_pass2_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ double2 lattdse_smem[];
-  constexpr int TS = B * SmemGeom<L, B>::LS;
+  constexpr int TS = SmemGeom<L, B>::bytes / 16;  // one tile incl. its ping-pong partner
   double2* data[2] = {lattdse_smem, lattdse_smem + TS};
   double2* dg[2] = {lattdse_smem + 2 * TS, lattdse_smem + 2 * TS + B * L};
   int t = blockIdx.x;

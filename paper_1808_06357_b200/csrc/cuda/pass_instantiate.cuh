@@ -20,7 +20,7 @@ template <int AXIS, int L> struct Geometry {
                                                        : (L >= LATTDSE_COL_B1_MIN ? 1 : (L >= 512 ? 2 : (L >= 128 ? 4 : 8)));
   static constexpr int raw = B * lattdse_dev::Plan<L>::max_tasks();
   static constexpr int NT = raw <= 32 ? 32 : (raw >= 512 ? 512 : ((raw + 31) / 32) * 32);
-  static constexpr int smem2 = 2 * lattdse_dev::SmemGeom<L, B>::bytes + 2 * B * L * 16;
+  static constexpr int smem2 = 2 * lattdse_dev::SmemGeom<L, B>::bytes + 2 * B * L * 16;  // v2 (opt-in)
 };
 
 template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
