@@ -327,6 +327,55 @@ def run_ours(args, cfg):
     return 0
 
 
+# ------------------------------------------------------------- sharded arm
+def run_sharded(args, cfg):
+    """One wave function sharded over the ranks (DistSolver): NCCL exchanges
+    between GPUs under torchrun, or --virtual-ranks G on one GPU."""
+    world, rank, local, dist, torch = dist_setup(args.gpus)
+    import paper_1808_06357_b200 as L
+    from paper_1808_06357_b200 import configs
+
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg, batch=1)
+    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    if world > 1:
+        uid = [L.DistSolver.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        D = L.DistSolver(lat, cfg.eps, a, b, c, p, cfg.sigma, world=world, rank=rank, device=local,
+                         nccl_id=uid[0], norm2=norm2)
+        G = world
+    else:
+        G = max(1, args.virtual_ranks)
+        D = L.DistSolver(lat, cfg.eps, a, b, c, p, cfg.sigma, world=G, rank=-1, device=0, norm2=norm2)
+    D.set_dt(cfg.dt)
+    D.discretize_initial()
+    m = cfg.m if args.m is None else args.m
+    for _ in range(args.warmup):
+        D.step(m)
+    barrier(dist)
+    per = [D.time_steps(m) for _ in range(args.steps)]
+    barrier(dist)
+    total_ms = max_over_ranks(sum(per), dist, torch)
+    norm = D.l2_norm()
+    info = D.info()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": float(cfg.N) * m * args.steps / (total_ms * 1e-3), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (complex fp64)",
+            "data": "synthetic (seeded BASELINE families, DESIGN.md Seeds)",
+            "config": {**config_dict(cfg, args), "parallelism": f"one wave function sharded over {G} ranks "
+                       f"({'NCCL send/recv' if world > 1 else 'virtual ranks on one GPU, device copies'}), "
+                       "2 block exchanges per Strang step"},
+            "sharded": {**info, "ranks": G, "norm_after": norm},
+            "us_per_strang_step": 1e3 * total_ms / (args.steps * m),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -340,6 +389,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-sample-steps", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", action="store_true", help="shard one wave function across the ranks (NCCL)")
+    ap.add_argument("--virtual-ranks", type=int, default=0, help="sharded path with G virtual ranks on one GPU")
     args = ap.parse_args()
     from paper_1808_06357_b200 import configs
 
@@ -348,6 +399,8 @@ def main():
         print("warning: the timing rules ask for >= 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.shard or args.virtual_ranks > 0:
+        return run_sharded(args, cfg)
     return run_ours(args, cfg)
 
 

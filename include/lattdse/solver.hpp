@@ -28,6 +28,8 @@ struct SolverOptions {
   std::string method = "circulant";
   /// members stepped together while L2-resident; 0 = automatic.
   std::int64_t group = 0;
+  /// force the length-M view M1 x M2 (rank-1; 0 = automatic)
+  std::int64_t force_M1 = 0, force_M2 = 0;
 };
 
 struct ProblemSpec {
@@ -94,6 +96,11 @@ class Solver {
 
   SolverInfo info() const;
   std::int64_t kernel_launches() const;  // pass + aux kernels launched so far
+
+  /// Device pointers of the propagator tables (for the sharded solver):
+  /// 0 = K^ (ROW-pass order, M entries), 1 = V (kappa order, N), 2 = V^(1/2) (N).
+  const void* device_table(int which) const;
+  int device() const;
 
  private:
   struct Impl;

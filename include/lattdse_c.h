@@ -143,6 +143,26 @@ int lattdse_solver_kernel_launches(lattdse_solver* s, int64_t* out);
 /* wait for all work queued on the solver stream */
 int lattdse_solver_synchronize(lattdse_solver* s);
 
+/* ---- sharded single wave function (SURVEY.md §8(e), config 4 strategy) --
+ * world ranks; rank = -1 runs all ranks as virtual ranks on `device` (block
+ * exchanges by device copies), rank >= 0 is one process per GPU with NCCL
+ * grouped send/recv (nccl_id from lattdse_dist_nccl_unique_id on rank 0). */
+typedef struct lattdse_dist lattdse_dist;
+int lattdse_dist_nccl_unique_id(uint8_t* out128);
+int lattdse_dist_create(const lattdse_lattice* lat, const uint32_t* norm2, const lattdse_problem* prob, int world,
+                        int rank, int device, const uint8_t* nccl_id, lattdse_dist** out);
+void lattdse_dist_destroy(lattdse_dist* d);
+int lattdse_dist_set_dt(lattdse_dist* d, double dt);
+int lattdse_dist_discretize_initial(lattdse_dist* d);
+/* full kappa-order sample vectors (N complex128); NCCL ranks touch only theirs */
+int lattdse_dist_set_state(lattdse_dist* d, const double* c128);
+int lattdse_dist_get_state(lattdse_dist* d, double* c128);
+int lattdse_dist_step(lattdse_dist* d, int64_t nsteps);
+int lattdse_dist_l2_norm(lattdse_dist* d, double* out);
+int lattdse_dist_time_steps(lattdse_dist* d, int64_t nsteps, double* ms);
+/* M, M1, M2 of the sharded view; bytes each rank sends per exchange (2/step) */
+int lattdse_dist_info(lattdse_dist* d, int64_t* M, int64_t* M1, int64_t* M2, double* exchange_bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -360,6 +360,76 @@ class Solver:
         return v.value
 
 
+class DistSolver:
+    """One wave function sharded over `world` ranks (include/lattdse/dist.hpp).
+    rank=-1: all ranks virtual on `device` (block exchanges by device copies);
+    rank>=0: one process per GPU, NCCL exchanges (nccl_id from rank 0)."""
+
+    def __init__(self, lat: Lattice, eps: float, a, b, c, p, sigma: float, *, world: int, rank: int = -1,
+                 device: int = 0, nccl_id: bytes | None = None, norm2=None):
+        self.lat = lat
+        d = lat.dim()
+        self._a = np.ascontiguousarray(a, np.float64)
+        self._b = np.ascontiguousarray(b if d > 1 else [0.0], np.float64)
+        self._c = np.ascontiguousarray(np.asarray(c, np.float64).reshape(-1, d)[:1])
+        self._p = np.ascontiguousarray(np.asarray(p, np.int32).reshape(-1, d)[:1])
+        self.n = lat.n_total()
+        prob = _Problem(eps, d, _ptr(self._a, C.c_double), _ptr(self._b, C.c_double), 1, sigma,
+                        _ptr(self._c, C.c_double), _ptr(self._p, C.c_int))
+        nv = None if norm2 is None else np.ascontiguousarray(norm2, np.uint32)
+        idb = None if nccl_id is None else (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        h = C.c_void_p()
+        _ck(_lib.lattdse_dist_create(lat.handle, _ptr(nv, C.c_uint32) if nv is not None else None, C.byref(prob),
+                                     world, rank, device, idb, C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _ck(_lib.lattdse_dist_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.lattdse_dist_destroy(h)
+            self._h = None
+
+    def set_dt(self, dt: float):
+        _ck(_lib.lattdse_dist_set_dt(self._h, C.c_double(dt)))
+
+    def discretize_initial(self):
+        _ck(_lib.lattdse_dist_discretize_initial(self._h))
+
+    def set_state(self, x):
+        x = np.ascontiguousarray(x, np.complex128).reshape(-1)
+        _ck(_lib.lattdse_dist_set_state(self._h, x.ctypes.data_as(dblp)))
+
+    def get_state(self) -> np.ndarray:
+        out = np.zeros(self.n, np.complex128)
+        _ck(_lib.lattdse_dist_get_state(self._h, out.ctypes.data_as(dblp)))
+        return out
+
+    def step(self, nsteps: int = 1):
+        _ck(_lib.lattdse_dist_step(self._h, C.c_int64(nsteps)))
+
+    def l2_norm(self) -> float:
+        v = C.c_double()
+        _ck(_lib.lattdse_dist_l2_norm(self._h, C.byref(v)))
+        return v.value
+
+    def time_steps(self, nsteps: int) -> float:
+        v = C.c_double()
+        _ck(_lib.lattdse_dist_time_steps(self._h, C.c_int64(nsteps), C.byref(v)))
+        return v.value
+
+    def info(self) -> dict:
+        M, M1, M2 = C.c_int64(), C.c_int64(), C.c_int64()
+        xb = C.c_double()
+        _ck(_lib.lattdse_dist_info(self._h, C.byref(M), C.byref(M1), C.byref(M2), C.byref(xb)))
+        return {"M": M.value, "M1": M1.value, "M2": M2.value, "exchange_bytes_per_rank": xb.value}
+
+
 def exported_symbols() -> list[str]:
     """Every lattdse_* function declared in include/lattdse_c.h."""
     import re

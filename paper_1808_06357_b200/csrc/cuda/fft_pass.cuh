@@ -67,6 +67,15 @@ struct PassArgs {
   int pfa;
   int pM1, pM2;
   long long pM;
+  // Sharded (distributed) layouts. COL pass on a column slab: storage row
+  // length ncols (slab width), global column = col_off + local column,
+  // natural index i*ncols_g + global column. ROW pass on a block-major row
+  // slab: a row is rb_n blocks of rb_w elements, block q of row r at
+  // q*rb_stride + r*rb_w (rb_w = 0: plain contiguous rows).
+  int col_off;
+  int ncols_g;
+  int rb_w, rb_n;
+  long long rb_stride;
 };
 
 // Shared-memory slots of one tile: B lines, each Plan<L>::phys-swizzled and
@@ -99,7 +108,13 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
 
   // array position of element (b, i) in the 2-D view
   LD_HD long long pos(int b, int i) const {
-    if (AXIS == AX_ROW) return (long long)(line0 + b) * L + i;
+    if (AXIS == AX_ROW) {
+      if (a.rb_w > 0) {
+        const int q = i / a.rb_w;
+        return (long long)q * a.rb_stride + (long long)(line0 + b) * a.rb_w + (i - q * a.rb_w);
+      }
+      return (long long)(line0 + b) * L + i;
+    }
     return (long long)i * a.ncols + (line0 + b);
   }
   // natural (sample / coefficient) index of element (b, i)
@@ -108,6 +123,7 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
       long long n = (long long)a.pM2 * i + (long long)a.pM1 * (line0 + b);
       return n >= a.pM ? n - a.pM : n;
     }
+    if (AXIS == AX_COL && a.ncols_g > 0) return (long long)i * a.ncols_g + (a.col_off + line0 + b);
     return pos(b, i);
   }
   // the compact (natural-order) side of single-transform programs
@@ -117,7 +133,7 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
     const long long mask = (1LL << a.tw_shift) - 1;
     return c_mul(a.tw_hi[t >> a.tw_shift], a.tw_lo[t & mask]);
   }
-  LD_HD long long tw_index(int b, int i) const { return (long long)(line0 + b) * i; }
+  LD_HD long long tw_index(int b, int i) const { return (long long)(a.col_off + line0 + b) * i; }
   LD_HD double2 apply_diag(double2 v, long long j) const {
     switch (a.diag_kind) {
       case DG_CPLX: return c_mul(v, a.diag[j]);
@@ -229,7 +245,7 @@ struct Stage {
   // four-step twiddles W(col * (j + r*T)) = W(col*j) * W(col*T)^r for the
   // elements j + r*T a task touches in stage 0 / the last stage
   LD_HD static void fourstep(const C& c, int b, int j, double2 (&v)[R], bool conj) {
-    const long long col = c.line0 + b;
+    const long long col = c.a.col_off + c.line0 + b;
     const double2 base = c.twid(col * j);
     Pow<R> pw;
     pw.init(c.twid(col * T), R > 4 ? c.twid(col * 4 * T) : make_double2(1.0, 0.0),

@@ -4,6 +4,9 @@
 #include "fft_pass.cuh"
 #include "pass_registry.hpp"
 
+#ifndef LATTDSE_BUILD_V2
+#define LATTDSE_BUILD_V2 0  // persistent double-buffered variant (opt-in, slower today)
+#endif
 #ifndef LATTDSE_COL_B1_MIN
 #define LATTDSE_COL_B1_MIN 4096  // columns this long: one column per CTA (smem for 3 CTAs/SM)
 #endif
@@ -36,14 +39,14 @@ template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
     k.fn_mb[1] = k.fn;
     k.fn_mb[2] = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN, 2>);
     k.fn_mb[3] = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN, 3>);
-    k.fn_mb[4] = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN, 4>);
+    k.fn_mb[4] = nullptr;  // measured never best (spills); not instantiated to keep the library small
     // measured on C1 (profiles/README.md): 3 resident CTAs/SM balance register
     // caps (small L1-resident spills) against occupancy for 5-10 warp CTAs
     // ROW: 3 CTAs/SM; COL (four-step twiddle math in the fused stages) keeps
     // more registers at 2 CTAs/SM
     k.default_mb = G::NT > 320 ? 2 : (AXIS == lattdse_dev::AX_ROW ? 3 : 2);
   }
-  if constexpr (PROG == lattdse_dev::PROG_DOUBLE && G::smem2 <= 227 * 1024) {
+  if constexpr (LATTDSE_BUILD_V2 && PROG == lattdse_dev::PROG_DOUBLE && G::smem2 <= 227 * 1024) {
     k.fn2 = reinterpret_cast<const void*>(&lattdse_dev::fft_pass2_kernel<AXIS, L, G::B, G::NT, SIGN>);
     k.smem2 = G::smem2;
   }

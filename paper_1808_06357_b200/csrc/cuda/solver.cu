@@ -232,6 +232,7 @@ struct Solver::Impl {
   long long M = 0, M1 = 0, M2 = 0;  // work = M1 rows x M2 cols
   int tw_shift = 0;
   bool pfa = false;                 // Good-Thomas layout (rank-1), else four-step
+  long long forced_M1 = 0, forced_M2 = 0;
 
   // device
   int device = 0;
@@ -469,6 +470,17 @@ struct Solver::Impl {
       return;
     }
     const long long need = 2 * N - 1;
+    if (forced_M1 > 0 && forced_M2 > 0) {
+      if (forced_M1 * forced_M2 < need || !dev::find_pass_kernel(AX_COL, (int)forced_M1, PROG_DOUBLE, -1) ||
+          !dev::find_pass_kernel(AX_ROW, (int)forced_M2, PROG_DOUBLE, -1))
+        raise(Errc::unsupported, "forced geometry " + std::to_string(forced_M1) + "x" + std::to_string(forced_M2) +
+                                     " is not compiled or too small for N=" + std::to_string(N));
+      M1 = forced_M1;
+      M2 = forced_M2;
+      M = M1 * M2;
+      pfa = false;
+      return;
+    }
     if (const char* g = std::getenv("LATTDSE_GEOM")) {  // "M1xM2" override (experiments)
       long long g1 = 0, g2 = 0;
       if (std::sscanf(g, "%lldx%lld", &g1, &g2) == 2 && g1 * g2 >= need && dev::find_pass_kernel(AX_COL, (int)g1, PROG_DOUBLE, -1) &&
@@ -815,6 +827,8 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
     raise(Errc::invalid_argument, "method must be 'circulant' or 'bluestein'");
   s.max_norm2 = aa.max_norm2;
   s.device = opt.device;
+  s.forced_M1 = opt.force_M1;
+  s.forced_M2 = opt.force_M2;
   LD_CK(cudaSetDevice(s.device));
   LD_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
   LD_CK(cudaDeviceGetAttribute(&s.num_sms, cudaDevAttrMultiProcessorCount, s.device));
@@ -1075,5 +1089,16 @@ SolverInfo Solver::info() const {
 }
 
 std::int64_t Solver::kernel_launches() const { return p_->launches; }
+
+const void* Solver::device_table(int which) const {
+  switch (which) {
+    case 0: return p_->Khat.p;
+    case 1: return p_->V.p;
+    case 2: return p_->Vh.p;
+    default: return nullptr;
+  }
+}
+
+int Solver::device() const { return p_->device; }
 
 }  // namespace lattdse

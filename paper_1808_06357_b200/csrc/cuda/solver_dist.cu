@@ -1,0 +1,526 @@
+// Sharded single-wave-function Strang stepping (include/lattdse/dist.hpp).
+//
+// Layouts per rank g (G ranks, M = M1*M2, Hb = M1/G, Wb = M2/G):
+//   column slab  A_g, S_g, V_g, Vh_g : M1 x Wb row-major, global columns
+//                                      [g*Wb, (g+1)*Wb), zeros where the
+//                                      natural index j1*M2 + col >= N
+//   row slab     B_g, K_g            : G blocks q of Hb x Wb (block-major):
+//                                      rows [g*Hb, (g+1)*Hb), columns of
+//                                      block q = [q*Wb, (q+1)*Wb)
+// Exchange col->row: A_g block h (rows of h, contiguous) -> B_h block g.
+// Exchange row->col: B_h block g -> A_g block h. Both sides contiguous, so
+// the NCCL path is G grouped send/recv pairs with no pack/unpack kernels.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+
+#include "fft_pass.cuh"
+#include "lattdse/dist.hpp"
+#include "pass_registry.hpp"
+
+using namespace lattdse_dev;
+
+namespace lattdse {
+
+#define LD_CK(x)                                                                                      \
+  do {                                                                                                \
+    cudaError_t e_ = (x);                                                                             \
+    if (e_ != cudaSuccess) raise(Errc::device_error, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+namespace {
+
+// ---------------------------------------------------------------- NCCL
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+  static Nccl& get() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      // the process's NCCL (e.g. torch's) if already loaded, else the system one
+      for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+        n.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+        if (n.h) break;
+      }
+      if (!n.h) return;
+      auto sym = [&](auto& fp, const char* s) { fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(n.h, s)); };
+      sym(n.GetUniqueId, "ncclGetUniqueId");
+      sym(n.CommInitRank, "ncclCommInitRank");
+      sym(n.CommDestroy, "ncclCommDestroy");
+      sym(n.GroupStart, "ncclGroupStart");
+      sym(n.GroupEnd, "ncclGroupEnd");
+      sym(n.Send, "ncclSend");
+      sym(n.Recv, "ncclRecv");
+      sym(n.AllReduce, "ncclAllReduce");
+      sym(n.GetErrorString, "ncclGetErrorString");
+    });
+    if (!n.h || !n.CommInitRank || !n.Send || !n.Recv)
+      raise(Errc::nccl_error, "libnccl.so.2 not found or incomplete (dlopen)");
+    return n;
+  }
+};
+
+#define LD_NCCL(x)                                                                                  \
+  do {                                                                                              \
+    ncclResult_t r_ = (x);                                                                          \
+    if (r_ != ncclSuccess) raise(Errc::nccl_error, std::string(#x) + ": " + Nccl::get().GetErrorString(r_)); \
+  } while (0)
+
+// --------------------------------------------------------------- kernels
+__global__ void k_colslab(const double2* __restrict__ src, long long N, long long M1, long long M2, long long Wb,
+                          long long col_off, double2* __restrict__ out) {
+  const long long n = M1 * Wb;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const long long j1 = p / Wb, c = p - j1 * Wb;
+    const long long j = j1 * M2 + col_off + c;
+    out[p] = j < N ? src[j] : make_double2(0.0, 0.0);
+  }
+}
+__global__ void k_slab2nat(const double2* __restrict__ slab, long long N, long long M1, long long M2, long long Wb,
+                           long long col_off, double2* __restrict__ dst) {
+  const long long n = M1 * Wb;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const long long j1 = p / Wb, c = p - j1 * Wb;
+    const long long j = j1 * M2 + col_off + c;
+    if (j < N) dst[j] = slab[p];
+  }
+}
+__global__ void k_rowblk(const double2* __restrict__ src, long long M2, long long Hb, long long Wb, int G,
+                         long long row_off, double2* __restrict__ out) {
+  const long long n = (long long)G * Hb * Wb;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const long long q = p / (Hb * Wb), rem = p - q * Hb * Wb, r = rem / Wb, c = rem - r * Wb;
+    out[p] = src[(row_off + r) * M2 + q * Wb + c];
+  }
+}
+__global__ void k_sumsq(const double2* __restrict__ x, long long n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    acc += x[i].x * x[i].x + x[i].y * x[i].y;
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) out[blockIdx.x] = acc;
+  }
+}
+
+template <class T> struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (p && n == count) return;
+    release();
+    if (count == 0) return;
+    LD_CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+};
+
+const long double kPiL = 3.141592653589793238462643383279502884L;
+
+std::vector<double2> roots(long long n, long long count, long long stride) {
+  std::vector<double2> t(count);
+  for (long long i = 0; i < count; ++i) {
+    long long q = (i * stride) % n;
+    long double a = -2.0L * kPiL * (long double)q / (long double)n;
+    t[i] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  return t;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ Impl
+struct DistSolver::Impl {
+  int G = 2, rank = -1, device = 0;
+  long long N = 0, M = 0, M1 = 0, M2 = 0, Hb = 0, Wb = 0;
+  cudaStream_t stream = nullptr;
+  std::unique_ptr<Solver> full;  // builds the propagator tables (forced geometry)
+  Lattice lat;
+  ProblemSpec prob;
+  std::vector<int> local;        // ranks living in this process
+  struct Rank {
+    DBuf<double2> A, B, S, V, Vh, K;
+  };
+  std::vector<Rank> rk;          // indexed like `local`
+  DBuf<double2> tw_col, tw_row, tw_col2, tw_row2, tw_lo, tw_hi, tmp;
+  DBuf<double> partial;
+  int tw_shift = 0;
+  ncclComm_t comm = nullptr;
+  bool have_dt = false;
+
+  explicit Impl(const Lattice& l) : lat(l) {}
+
+  int grid1d(long long n) const { return (int)std::min<long long>((n + 255) / 256, 148 * 16); }
+
+  void launch(int axis, int L, int prog, int sign, PassArgs a, long long nlines) {
+    dev::PassKernel* k = dev::find_pass_kernel(axis, L, prog, sign);
+    if (!k) raise(Errc::unsupported, "no pass kernel for L=" + std::to_string(L));
+    const void* fn = k->fn;
+    if (prog == PROG_DOUBLE && k->fn_mb[k->default_mb]) fn = k->fn_mb[k->default_mb];
+    if (!k->attr_set) {
+      for (int m = 0; m <= 4; ++m) {
+        const void* f = m == 0 ? k->fn : k->fn_mb[m];
+        if (f) LD_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem));
+      }
+      k->attr_set = true;
+    }
+    a.nlines = (int)nlines;
+    void* args[] = {&a};
+    LD_CK(cudaLaunchKernel(fn, dim3((unsigned)((nlines + k->B - 1) / k->B), 1), dim3(k->NT), args, (size_t)k->smem,
+                           stream));
+  }
+
+  PassArgs col_args(int g) const {
+    PassArgs a{};
+    a.ncols = (int)Wb;
+    a.col_off = (int)(g * Wb);
+    a.fft_tw = tw_col.p;
+    a.fft_tw2 = tw_col2.p;
+    a.tw_lo = tw_lo.p;
+    a.tw_hi = tw_hi.p;
+    a.tw_shift = tw_shift;
+    a.in_bstride = a.out_bstride = M1 * Wb;
+    a.nvalid_in = a.nvalid_mid = a.nvalid_out = M1 * Wb;  // masks folded into the slab tables
+    a.diag_kind = DG_CPLX;
+    return a;
+  }
+  PassArgs row_args() const {
+    PassArgs a{};
+    a.ncols = (int)M2;
+    a.fft_tw = tw_row.p;
+    a.fft_tw2 = tw_row2.p;
+    a.in_bstride = a.out_bstride = Hb * M2;
+    a.nvalid_in = a.nvalid_mid = a.nvalid_out = Hb * M2;
+    a.rb_w = (int)Wb;
+    a.rb_n = G;
+    a.rb_stride = Hb * Wb;
+    a.diag_kind = DG_CPLX;
+    return a;
+  }
+
+  void upload_twiddles() {
+    auto up = [&](DBuf<double2>& b, const std::vector<double2>& h) {
+      b.alloc(h.size());
+      LD_CK(cudaMemcpy(b.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    };
+    auto stage_tw = [&](int axis, long long L, bool rev) {
+      const dev::PassKernel* k = dev::find_pass_kernel(axis, (int)L, PROG_DOUBLE, -1);
+      int radix[16];
+      for (int s = 0; s < k->nst; ++s) radix[s] = k->radix[rev ? k->nst - 1 - s : s];
+      std::vector<double2> t(std::max(1, build_stage_twiddles(radix, k->nst, nullptr)), make_double2(1.0, 0.0));
+      build_stage_twiddles(radix, k->nst, t.data());
+      return t;
+    };
+    up(tw_col, stage_tw(AX_COL, M1, false));
+    up(tw_col2, stage_tw(AX_COL, M1, true));
+    up(tw_row, stage_tw(AX_ROW, M2, false));
+    up(tw_row2, stage_tw(AX_ROW, M2, true));
+    tw_shift = 0;
+    while ((1LL << (2 * tw_shift)) < M) ++tw_shift;
+    const long long nlo = 1LL << tw_shift, nhi = (M + nlo - 1) / nlo;
+    up(tw_lo, roots(M, nlo, 1));
+    up(tw_hi, roots(M, nhi, nlo));
+  }
+
+  // choose M1 x M2 >= 2N-1 with G | M1, G | M2 among the compiled lengths
+  void choose_geometry() {
+    const long long need = 2 * N - 1;
+    long long best = -1;
+    double bal = 0;
+    for (int L1 : dev::pass_lengths(AX_COL))
+      for (int L2 : dev::pass_lengths(AX_ROW)) {
+        const long long m = (long long)L1 * L2;
+        if (m < need || L1 % G || L2 % G) continue;
+        const double bl = std::fabs(std::log((double)L1 / L2));
+        if (best < 0 || m < best || (m == best && bl < bal)) {
+          best = m;
+          bal = bl;
+          M1 = L1;
+          M2 = L2;
+        }
+      }
+    if (best < 0) raise(Errc::unsupported, "no compiled M1 x M2 divisible by G=" + std::to_string(G));
+    M = best;
+    Hb = M1 / G;
+    Wb = M2 / G;
+  }
+
+  void exchange(bool col_to_row) {
+    const long long blk = Hb * Wb;
+    if (rank < 0) {  // virtual ranks: device copies
+      for (int g = 0; g < G; ++g)
+        for (int h = 0; h < G; ++h) {
+          // col->row: A_g block h -> B_h block g ; row->col: B_h block g -> A_g block h
+          if (col_to_row)
+            LD_CK(cudaMemcpyAsync(rk[h].B.p + g * blk, rk[g].A.p + h * blk, blk * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, stream));
+          else
+            LD_CK(cudaMemcpyAsync(rk[g].A.p + h * blk, rk[h].B.p + g * blk, blk * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, stream));
+        }
+      return;
+    }
+    Nccl& n = Nccl::get();
+    const int g = rank;
+    Rank& R = rk[0];
+    LD_NCCL(n.GroupStart());
+    for (int h = 0; h < G; ++h) {
+      if (h == g) continue;
+      if (col_to_row) {
+        LD_NCCL(n.Send(R.A.p + h * blk, 2 * blk, ncclDouble, h, comm, stream));
+        LD_NCCL(n.Recv(R.B.p + h * blk, 2 * blk, ncclDouble, h, comm, stream));
+      } else {
+        LD_NCCL(n.Send(R.B.p + h * blk, 2 * blk, ncclDouble, h, comm, stream));
+        LD_NCCL(n.Recv(R.A.p + h * blk, 2 * blk, ncclDouble, h, comm, stream));
+      }
+    }
+    LD_NCCL(n.GroupEnd());
+    if (col_to_row)
+      LD_CK(cudaMemcpyAsync(R.B.p + g * blk, R.A.p + g * blk, blk * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+    else
+      LD_CK(cudaMemcpyAsync(R.A.p + g * blk, R.B.p + g * blk, blk * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+  }
+
+  void col_entry(int i) {
+    const int g = local[i];
+    PassArgs a = col_args(g);
+    a.in = rk[i].S.p;
+    a.out = rk[i].A.p;
+    a.diag = rk[i].Vh.p;
+    a.post_tw = 1;
+    launch(AX_COL, (int)M1, PROG_LOADDIAG, -1, a, Wb);
+  }
+  void col_mid(int i) {
+    const int g = local[i];
+    PassArgs a = col_args(g);
+    a.in = a.out = rk[i].A.p;
+    a.diag = rk[i].V.p;
+    a.pre_tw = a.post_tw = 1;
+    launch(AX_COL, (int)M1, PROG_DOUBLE, +1, a, Wb);
+  }
+  void col_exit(int i) {
+    const int g = local[i];
+    PassArgs a = col_args(g);
+    a.in = rk[i].A.p;
+    a.out = rk[i].S.p;
+    a.diag = rk[i].Vh.p;
+    a.pre_tw = 1;
+    launch(AX_COL, (int)M1, PROG_STOREDIAG, +1, a, Wb);
+  }
+  void row_mid(int i) {
+    PassArgs a = row_args();
+    a.in = a.out = rk[i].B.p;
+    a.diag = rk[i].K.p;
+    launch(AX_ROW, (int)M2, PROG_DOUBLE, -1, a, Hb);
+  }
+
+  void enqueue_steps(long long n) {
+    if (!have_dt) raise(Errc::config_error, "set_dt must be called before stepping");
+    if (n <= 0) return;
+    const int nl = (int)local.size();
+    for (int i = 0; i < nl; ++i) col_entry(i);
+    for (long long k = 0; k < n; ++k) {
+      exchange(true);
+      for (int i = 0; i < nl; ++i) row_mid(i);
+      exchange(false);
+      for (int i = 0; i < nl; ++i) {
+        if (k + 1 < n)
+          col_mid(i);
+        else
+          col_exit(i);
+      }
+    }
+    LD_CK(cudaGetLastError());
+  }
+};
+
+// --------------------------------------------------------------- DistSolver
+DistSolver::DistSolver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& prob, const DistOptions& opt)
+    : p_(std::make_unique<Impl>(lat)) {
+  Impl& s = *p_;
+  if (lat.rank() != 1) raise(Errc::unsupported, "the sharded solver handles rank-1 lattices");
+  if (prob.initial.size() != 1) raise(Errc::invalid_argument, "the sharded solver steps one wave function");
+  if (opt.world < 1) raise(Errc::invalid_argument, "world must be >= 1");
+  if (opt.rank >= opt.world) raise(Errc::invalid_argument, "rank must be < world");
+  s.G = opt.world;
+  s.rank = opt.rank;
+  s.device = opt.device;
+  s.N = lat.n_total();
+  s.prob = prob;
+  LD_CK(cudaSetDevice(s.device));
+  LD_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+  s.choose_geometry();
+  SolverOptions so;
+  so.device = s.device;
+  so.force_M1 = s.M1;
+  so.force_M2 = s.M2;
+  so.group = 1;
+  s.full = std::make_unique<Solver>(lat, aa, prob, so);
+  s.upload_twiddles();
+  if (s.rank < 0)
+    for (int g = 0; g < s.G; ++g) s.local.push_back(g);
+  else
+    s.local.push_back(s.rank);
+  s.rk.resize(s.local.size());
+  const size_t slab = (size_t)(s.M1 * s.Wb);
+  for (auto& r : s.rk) {
+    r.A.alloc(slab);
+    r.B.alloc(slab);
+    r.S.alloc(slab);
+    r.V.alloc(slab);
+    r.Vh.alloc(slab);
+    r.K.alloc(slab);
+    LD_CK(cudaMemset(r.S.p, 0, slab * sizeof(double2)));
+  }
+  if (s.rank >= 0 && s.G > 1) {
+    if (!opt.nccl_id) raise(Errc::invalid_argument, "NCCL mode needs the rank-0 unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, opt.nccl_id, sizeof id);
+    LD_NCCL(Nccl::get().CommInitRank(&s.comm, s.G, id, s.rank));
+  }
+}
+
+DistSolver::~DistSolver() {
+  if (!p_) return;
+  if (p_->stream) cudaStreamSynchronize(p_->stream);
+  if (p_->comm) Nccl::get().CommDestroy(p_->comm);
+  if (p_->stream) cudaStreamDestroy(p_->stream);
+}
+
+void DistSolver::nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  LD_NCCL(Nccl::get().GetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof id);
+}
+
+void DistSolver::set_dt(double dt) {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  s.full->set_dt(dt);
+  const auto* K = (const double2*)s.full->device_table(0);
+  const auto* V = (const double2*)s.full->device_table(1);
+  const auto* Vh = (const double2*)s.full->device_table(2);
+  const long long slab = s.M1 * s.Wb;
+  for (size_t i = 0; i < s.local.size(); ++i) {
+    const int g = s.local[i];
+    k_colslab<<<s.grid1d(slab), 256, 0, s.stream>>>(V, s.N, s.M1, s.M2, s.Wb, g * s.Wb, s.rk[i].V.p);
+    k_colslab<<<s.grid1d(slab), 256, 0, s.stream>>>(Vh, s.N, s.M1, s.M2, s.Wb, g * s.Wb, s.rk[i].Vh.p);
+    k_rowblk<<<s.grid1d(slab), 256, 0, s.stream>>>(K, s.M2, s.Hb, s.Wb, s.G, g * s.Hb, s.rk[i].K.p);
+  }
+  LD_CK(cudaStreamSynchronize(s.stream));
+  LD_CK(cudaGetLastError());
+  s.have_dt = true;
+}
+
+void DistSolver::set_state(const std::complex<double>* samples) {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  s.tmp.alloc(s.N);
+  LD_CK(cudaMemcpyAsync(s.tmp.p, samples, s.N * sizeof(double2), cudaMemcpyHostToDevice, s.stream));
+  const long long slab = s.M1 * s.Wb;
+  for (size_t i = 0; i < s.local.size(); ++i)
+    k_colslab<<<s.grid1d(slab), 256, 0, s.stream>>>(s.tmp.p, s.N, s.M1, s.M2, s.Wb, s.local[i] * s.Wb, s.rk[i].S.p);
+  LD_CK(cudaStreamSynchronize(s.stream));
+}
+
+void DistSolver::discretize_initial() {
+  Impl& s = *p_;
+  problems::Initial g = s.prob.initial[0];
+  auto gv = problems::sample_g(s.lat, g);
+  set_state(gv.data());
+}
+
+void DistSolver::get_state(std::complex<double>* samples) {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  s.tmp.alloc(s.N);
+  LD_CK(cudaMemcpyAsync(s.tmp.p, samples, s.N * sizeof(double2), cudaMemcpyHostToDevice, s.stream));
+  const long long slab = s.M1 * s.Wb;
+  for (size_t i = 0; i < s.local.size(); ++i)
+    k_slab2nat<<<s.grid1d(slab), 256, 0, s.stream>>>(s.rk[i].S.p, s.N, s.M1, s.M2, s.Wb, s.local[i] * s.Wb, s.tmp.p);
+  LD_CK(cudaMemcpyAsync(samples, s.tmp.p, s.N * sizeof(double2), cudaMemcpyDeviceToHost, s.stream));
+  LD_CK(cudaStreamSynchronize(s.stream));
+}
+
+void DistSolver::step(std::int64_t nsteps) {
+  LD_CK(cudaSetDevice(p_->device));
+  p_->enqueue_steps(nsteps);
+  LD_CK(cudaStreamSynchronize(p_->stream));
+}
+
+double DistSolver::time_steps(std::int64_t nsteps) {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  cudaEvent_t a, b;
+  LD_CK(cudaEventCreate(&a));
+  LD_CK(cudaEventCreate(&b));
+  LD_CK(cudaEventRecord(a, s.stream));
+  s.enqueue_steps(nsteps);
+  LD_CK(cudaEventRecord(b, s.stream));
+  LD_CK(cudaEventSynchronize(b));
+  float ms = 0;
+  LD_CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return ms;
+}
+
+double DistSolver::l2_norm() {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  const long long slab = s.M1 * s.Wb;
+  const int blocks = 592;
+  s.partial.alloc((size_t)blocks * s.local.size() + 1);
+  for (size_t i = 0; i < s.local.size(); ++i)
+    k_sumsq<<<blocks, 256, 0, s.stream>>>(s.rk[i].S.p, slab, s.partial.p + i * blocks);
+  std::vector<double> h((size_t)blocks * s.local.size());
+  LD_CK(cudaMemcpyAsync(h.data(), s.partial.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+  LD_CK(cudaStreamSynchronize(s.stream));
+  long double tot = 0;
+  for (double x : h) tot += x;
+  double sum = (double)tot;
+  if (s.comm) {
+    LD_CK(cudaMemcpyAsync(s.partial.p, &sum, sizeof(double), cudaMemcpyHostToDevice, s.stream));
+    LD_NCCL(Nccl::get().AllReduce(s.partial.p, s.partial.p, 1, ncclDouble, ncclSum, s.comm, s.stream));
+    LD_CK(cudaMemcpyAsync(&sum, s.partial.p, sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+    LD_CK(cudaStreamSynchronize(s.stream));
+  }
+  return std::sqrt(sum / (double)s.N);
+}
+
+std::int64_t DistSolver::M() const { return p_->M; }
+std::int64_t DistSolver::M1() const { return p_->M1; }
+std::int64_t DistSolver::M2() const { return p_->M2; }
+int DistSolver::world() const { return p_->G; }
+double DistSolver::exchange_bytes_per_rank() const {
+  return 16.0 * (double)p_->Hb * (double)p_->Wb * (double)(p_->G - 1);
+}
+
+}  // namespace lattdse

@@ -6,6 +6,7 @@
 #include <new>
 #include <string>
 
+#include "lattdse/dist.hpp"
 #include "lattdse/lattice.hpp"
 #include "lattdse/setup.hpp"
 #include "lattdse/solver.hpp"
@@ -17,6 +18,9 @@ struct lattdse_lattice {
 struct lattdse_solver {
   std::unique_ptr<lattdse::Solver> s;
   std::int64_t batch = 1;
+};
+struct lattdse_dist {
+  std::unique_ptr<lattdse::DistSolver> d;
 };
 
 namespace {
@@ -457,6 +461,106 @@ int lattdse_solver_kernel_launches(lattdse_solver* s, int64_t* out) {
     LD_NEED_S();
     need(out, "out");
     *out = s->s->kernel_launches();
+  });
+}
+
+int lattdse_dist_nccl_unique_id(uint8_t* out128) {
+  return guard([&] {
+    need(out128, "out");
+    lattdse::DistSolver::nccl_unique_id(out128);
+  });
+}
+
+int lattdse_dist_create(const lattdse_lattice* lat, const uint32_t* norm2, const lattdse_problem* prob, int world,
+                        int rank, int device, const uint8_t* nccl_id, lattdse_dist** out) {
+  return guard([&] {
+    need(lat, "lattice");
+    need(out, "out");
+    auto ps = make_problem(prob);
+    lattdse::AntiAliasSet aa;
+    if (norm2) {
+      aa.n_total = lat->lat.n_total();
+      aa.dim = lat->lat.dim();
+      aa.norm2.assign(norm2, norm2 + aa.n_total);
+      for (auto x : aa.norm2) aa.max_norm2 = std::max(aa.max_norm2, x);
+    } else {
+      aa = lattdse::AntiAliasSet::build(lat->lat, false);
+    }
+    lattdse::DistOptions o;
+    o.world = world;
+    o.rank = rank;
+    o.device = device;
+    o.nccl_id = nccl_id;
+    auto* h = new lattdse_dist;
+    try {
+      h->d = std::make_unique<lattdse::DistSolver>(lat->lat, aa, ps, o);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void lattdse_dist_destroy(lattdse_dist* d) { delete d; }
+
+#define LD_NEED_D() \
+  need(d, "dist");  \
+  need(d->d.get(), "dist")
+
+int lattdse_dist_set_dt(lattdse_dist* d, double dt) {
+  return guard([&] {
+    LD_NEED_D();
+    d->d->set_dt(dt);
+  });
+}
+int lattdse_dist_discretize_initial(lattdse_dist* d) {
+  return guard([&] {
+    LD_NEED_D();
+    d->d->discretize_initial();
+  });
+}
+int lattdse_dist_set_state(lattdse_dist* d, const double* c128) {
+  return guard([&] {
+    LD_NEED_D();
+    need(c128, "state");
+    d->d->set_state(reinterpret_cast<const std::complex<double>*>(c128));
+  });
+}
+int lattdse_dist_get_state(lattdse_dist* d, double* c128) {
+  return guard([&] {
+    LD_NEED_D();
+    need(c128, "state");
+    d->d->get_state(reinterpret_cast<std::complex<double>*>(c128));
+  });
+}
+int lattdse_dist_step(lattdse_dist* d, int64_t nsteps) {
+  return guard([&] {
+    LD_NEED_D();
+    d->d->step(nsteps);
+  });
+}
+int lattdse_dist_l2_norm(lattdse_dist* d, double* out) {
+  return guard([&] {
+    LD_NEED_D();
+    need(out, "out");
+    *out = d->d->l2_norm();
+  });
+}
+int lattdse_dist_time_steps(lattdse_dist* d, int64_t nsteps, double* ms) {
+  return guard([&] {
+    LD_NEED_D();
+    need(ms, "ms");
+    *ms = d->d->time_steps(nsteps);
+  });
+}
+int lattdse_dist_info(lattdse_dist* d, int64_t* M, int64_t* M1, int64_t* M2, double* exchange_bytes) {
+  return guard([&] {
+    LD_NEED_D();
+    if (M) *M = d->d->M();
+    if (M1) *M1 = d->d->M1();
+    if (M2) *M2 = d->d->M2();
+    if (exchange_bytes) *exchange_bytes = d->d->exchange_bytes_per_rank();
   });
 }
 

@@ -199,3 +199,42 @@ def test_config3_members_vs_oracle():
         _, _, u2 = oracle_coeffs(orc, c[m], p[m], cfg.sigma, 2)
         assert rel(got[m], u2) <= TOL_ONE * 2
     assert np.all(np.abs(S.l2_norm() - 1.0) <= TOL_NORM)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_virtual_ranks(world):
+    """Sharded single wave function (slabs + block exchanges) on `world`
+    virtual ranks of one GPU vs the unsharded solver and the oracle."""
+    lat, a, b, c, p = configs.small_rank1(4, 16411, seed=17)
+    eps, dt, sigma = 0.1, 1.0 / 64, 0.1
+    S, orc = make(lat, a, b, c, p, sigma, eps, dt)
+    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    D = L.DistSolver(lat, eps, a, b, c, p, sigma, world=world, rank=-1, norm2=norm2)
+    D.set_dt(dt)
+    D.discretize_initial()
+    assert rel(D.get_state(), S.get_state()[0]) <= 1e-15
+    D.step(1)
+    S.step(1)
+    g, u0, u1 = oracle_coeffs(orc, c[0], p[0], sigma, 1)
+    assert rel(orc.analyze(D.get_state()), u1) <= TOL_ONE
+    D.step(9)
+    S.step(9)
+    assert rel(D.get_state(), S.get_state()[0]) <= 1e-12
+    assert abs(D.l2_norm() - 1.0) <= TOL_NORM
+    assert D.info()["M1"] % world == 0 and D.info()["M2"] % world == 0
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_sharded_config1(world):
+    cfg = configs.CONFIGS["C1"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    S, orc = make(lat, a, b, c, p, cfg.sigma, cfg.eps, cfg.dt)
+    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    D = L.DistSolver(lat, cfg.eps, a, b, c, p, cfg.sigma, world=world, rank=-1, norm2=norm2)
+    D.set_dt(cfg.dt)
+    D.discretize_initial()
+    D.step(4)
+    S.step(4)
+    assert rel(D.get_state(), S.get_state()[0]) <= 1e-12
+    assert abs(D.l2_norm() - 1.0) <= TOL_NORM
