@@ -66,6 +66,7 @@ class Solver {
   /// Build the propagator phases for a time step.
   void set_dt(double dt);
   double dt() const;
+  void set_watchdog(double tol);
 
   /// g sampled on the lattice for every member; the state is
   /// held in sample space, so this is the discretised initial condition.
@@ -78,6 +79,8 @@ class Solver {
   /// nsteps Strang steps on every member.
   void step(std::int64_t nsteps);
   /// m steps with observables every record_every steps.
+  /// Raises numerical_invariant when |norm - norm(0)| at a record step exceeds
+  /// the watchdog tolerance (set_watchdog; default 1e-9, 0 = off).
   std::vector<TrajectoryRow> propagate(std::int64_t m, std::int64_t record_every, std::int64_t member = 0);
 
   std::vector<double> l2_norm();   // per member

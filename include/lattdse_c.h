@@ -134,6 +134,20 @@ int lattdse_solver_l2_distance(lattdse_solver* s, const double* c128, int space,
 int lattdse_solver_propagate(lattdse_solver* s, int64_t m, int64_t record_every, int64_t member, double* rows_out,
                              int64_t* nrows);
 int lattdse_solver_info_get(lattdse_solver* s, lattdse_solver_info* out);
+/* norm-drift watchdog of propagate: numerical_invariant (12) when
+ * |norm - norm(0)| > tol at a record step; default 1e-9, 0 disables */
+int lattdse_solver_set_watchdog(lattdse_solver* s, double tol);
+
+/* ---- state snapshots (include/lattdse/snapshot.hpp) -----
+ * `path` holds members*N little-endian complex128; `path`.json the sidecar
+ * (length, ordering, lattice + hash, step, time, dt). probe/read check the
+ * sidecar against `lat`: config_error (10) on mismatch, io_error (13) on
+ * missing/short files. space: 0 samples (kappa order), 1 coefficients (chi). */
+int lattdse_snapshot_write(const lattdse_lattice* lat, const char* path, const double* c128, int64_t members,
+                           int space, int64_t step, double time, double dt);
+int lattdse_snapshot_probe(const lattdse_lattice* lat, const char* path, int64_t* members, int* space,
+                           int64_t* step, double* time, double* dt);
+int lattdse_snapshot_read(const lattdse_lattice* lat, const char* path, double* c128, int64_t capacity);
 
 /* ---- measurement hooks (bench.py) -------------------------------------- */
 int lattdse_solver_time_steps(lattdse_solver* s, int64_t nsteps, double* ms);

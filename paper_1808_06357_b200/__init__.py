@@ -287,6 +287,24 @@ class Solver:
 
     def set_dt(self, dt: float):
         _ck(_lib.lattdse_solver_set_dt(self._h, C.c_double(dt)))
+        self.dt = float(dt)
+
+    def set_watchdog(self, tol: float):
+        """propagate raises numerical_invariant when |norm - norm(0)| > tol (0 = off)."""
+        _ck(_lib.lattdse_solver_set_watchdog(self._h, C.c_double(tol)))
+
+    def save(self, path: str, step: int = 0, time: float = 0.0, space: int = SAMPLES):
+        """Snapshot every member's state (checkpoint)."""
+        snapshot_write(self.lat, path, self.get_state(space), space=space, step=step, time=time,
+                       dt=getattr(self, "dt", 0.0))
+
+    def load(self, path: str) -> dict:
+        """Resume from a snapshot written for the same lattice and batch; returns its metadata."""
+        data, meta = snapshot_read(self.lat, path)
+        if data.shape[0] != self.batch:
+            raise LattdseError(10, f"snapshot holds {data.shape[0]} members, solver has {self.batch}")
+        self.set_state(data, meta["space"])
+        return meta
 
     def discretize_initial(self):
         _ck(_lib.lattdse_solver_discretize_initial(self._h))
@@ -428,6 +446,24 @@ class DistSolver:
         xb = C.c_double()
         _ck(_lib.lattdse_dist_info(self._h, C.byref(M), C.byref(M1), C.byref(M2), C.byref(xb)))
         return {"M": M.value, "M1": M1.value, "M2": M2.value, "exchange_bytes_per_rank": xb.value}
+
+
+def snapshot_write(lat: Lattice, path: str, data, *, space: int = SAMPLES, step: int = 0, time: float = 0.0,
+                   dt: float = 0.0):
+    """Raw little-endian complex128 + JSON sidecar (include/lattdse/snapshot.hpp)."""
+    x = np.ascontiguousarray(data, np.complex128).reshape(-1, lat.n_total())
+    _ck(_lib.lattdse_snapshot_write(lat.handle, os.fsencode(path), x.ctypes.data_as(dblp), C.c_int64(x.shape[0]),
+                                    space, C.c_int64(step), C.c_double(time), C.c_double(dt)))
+
+
+def snapshot_read(lat: Lattice, path: str):
+    """Returns (members x N complex128 array, metadata dict) after checking the sidecar against `lat`."""
+    mem, sp, st, t, dt = C.c_int64(), C.c_int(), C.c_int64(), C.c_double(), C.c_double()
+    _ck(_lib.lattdse_snapshot_probe(lat.handle, os.fsencode(path), C.byref(mem), C.byref(sp), C.byref(st),
+                                    C.byref(t), C.byref(dt)))
+    out = np.zeros((mem.value, lat.n_total()), np.complex128)
+    _ck(_lib.lattdse_snapshot_read(lat.handle, os.fsencode(path), out.ctypes.data_as(dblp), C.c_int64(out.size)))
+    return out, {"members": mem.value, "space": sp.value, "step": st.value, "time": t.value, "dt": dt.value}
 
 
 def exported_symbols() -> list[str]:

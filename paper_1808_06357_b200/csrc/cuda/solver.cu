@@ -222,6 +222,7 @@ struct Solver::Impl {
   long long N = 0, n1 = 0, n2 = 0;  // rank-2: grid n1 x n2
   long long batch = 1, group = 1;
   double eps = 1, dt_ = 0;
+  double watchdog_tol = 1e-9;  // propagate: max |norm - norm(0)| (0 = off)
   bool have_dt = false;
   std::string method;
   ProblemSpec prob;
@@ -895,6 +896,11 @@ void Solver::set_dt(double dt) {
 
 double Solver::dt() const { return p_->dt_; }
 
+void Solver::set_watchdog(double tol) {
+  if (!(tol >= 0)) raise(Errc::invalid_argument, "watchdog tolerance must be >= 0");
+  p_->watchdog_tol = tol;
+}
+
 void Solver::discretize_initial() {
   Impl& s = *p_;
   LD_CK(cudaSetDevice(s.device));
@@ -991,11 +997,17 @@ std::vector<TrajectoryRow> Solver::propagate(std::int64_t m, std::int64_t record
     rows.push_back({k, (double)k * p_->dt_, l2_norm()[member], energy()[member]});
   };
   record(0);
+  const double norm0 = rows[0].norm;
   for (std::int64_t k = 0; k < m;) {
     std::int64_t n = std::min(record_every, m - k);
     step(n);
     k += n;
     record(k);
+    // norm-drift watchdog (numerical_invariant, CLI exit code 3)
+    const double drift = std::fabs(rows.back().norm - norm0);
+    if (p_->watchdog_tol > 0 && !(drift <= p_->watchdog_tol))
+      raise(Errc::numerical_invariant, "norm drift " + std::to_string(drift) + " at step " + std::to_string(k) +
+                                           " exceeds " + std::to_string(p_->watchdog_tol));
   }
   return rows;
 }

@@ -9,6 +9,7 @@
 #include "lattdse/dist.hpp"
 #include "lattdse/lattice.hpp"
 #include "lattdse/setup.hpp"
+#include "lattdse/snapshot.hpp"
 #include "lattdse/solver.hpp"
 #include "lattdse_c.h"
 
@@ -409,6 +410,52 @@ int lattdse_solver_propagate(lattdse_solver* s, int64_t m, int64_t record_every,
         rows_out[4 * i + 2] = rows[i].norm;
         rows_out[4 * i + 3] = rows[i].energy;
       }
+  });
+}
+
+int lattdse_solver_set_watchdog(lattdse_solver* s, double tol) {
+  return guard([&] {
+    LD_NEED_S();
+    s->s->set_watchdog(tol);
+  });
+}
+
+int lattdse_snapshot_write(const lattdse_lattice* lat, const char* path, const double* c128, int64_t members,
+                           int space, int64_t step, double time, double dt) {
+  return guard([&] {
+    need(lat, "lattice");
+    need(path, "path");
+    need(c128, "data");
+    lattdse::SnapshotMeta m;
+    m.members = members;
+    m.space = space;
+    m.step = step;
+    m.time = time;
+    m.dt = dt;
+    lattdse::snapshot_write(path, lat->lat, reinterpret_cast<const std::complex<double>*>(c128), m);
+  });
+}
+
+int lattdse_snapshot_probe(const lattdse_lattice* lat, const char* path, int64_t* members, int* space,
+                           int64_t* step, double* time, double* dt) {
+  return guard([&] {
+    need(lat, "lattice");
+    need(path, "path");
+    auto m = lattdse::snapshot_probe(path, lat->lat);
+    if (members) *members = m.members;
+    if (space) *space = m.space;
+    if (step) *step = m.step;
+    if (time) *time = m.time;
+    if (dt) *dt = m.dt;
+  });
+}
+
+int lattdse_snapshot_read(const lattdse_lattice* lat, const char* path, double* c128, int64_t capacity) {
+  return guard([&] {
+    need(lat, "lattice");
+    need(path, "path");
+    need(c128, "data");
+    lattdse::snapshot_read(path, lat->lat, reinterpret_cast<std::complex<double>*>(c128), capacity);
   });
 }
 
