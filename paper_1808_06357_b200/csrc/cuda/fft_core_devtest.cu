@@ -111,13 +111,10 @@ int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin
 int main(int argc, char** argv) {
   int bad = 0;
   if (argc > 1 && std::string(argv[1]) == "time") {
-    run<AX_ROW, 1728, 1, 192, PROG_DOUBLE, -1, 3>(1215, 1728, 0, 0, -1, true);
-    run<AX_COL, 1215, 2, 288, PROG_DOUBLE, 1, 3>(1215, 1728, 1, 1, -1, true);
-    run<AX_COL, 1215, 2, 288, PROG_DOUBLE, 1, 3>(1215, 1728, 0, 0, -1, true);   // no four-step twiddles
-    run<AX_COL, 1215, 2, 288, PROG_DOUBLE, 1, 2>(1215, 1728, 1, 1, -1, true);
-    run<AX_ROW, 1728, 1, 192, PROG_DOUBLE, -1, 2>(1215, 1728, 0, 0, -1, true);
-    run<AX_ROW, 720, 1, 256, PROG_DOUBLE, -1, 3>(729, 720, 0, 0, -1, true);
-    run<AX_COL, 729, 2, 192, PROG_DOUBLE, 1, 3>(729, 720, 1, 1, -1, true);
+    // config-1 production geometry (1296 x 1620)
+    run<AX_ROW, 1620, 1, 192, PROG_DOUBLE, -1, 3>(1296, 1620, 0, 0, -1, true);
+    run<AX_COL, 1296, 2, 288, PROG_DOUBLE, 1, 2>(1296, 1620, 1, 1, -1, true);
+    run<AX_COL, 1296, 2, 288, PROG_DOUBLE, 1, 2>(1296, 1620, 0, 0, -1, true);  // no four-step twiddles
     return 0;
   }
   if (argc > 1) {

@@ -31,6 +31,9 @@
 #ifndef LATTDSE_PINGPONG
 #define LATTDSE_PINGPONG 1  // two shared buffers: stage s reads one, writes the other (1 barrier/stage)
 #endif
+#ifndef LATTDSE_MID_PREFETCH
+#define LATTDSE_MID_PREFETCH 1  // batch the mid-diagonal loads ahead of the fused mid stage
+#endif
 #ifndef LATTDSE_ABLATE
 #define LATTDSE_ABLATE 0  // devtest-only timing ablations: 1 mid diag, 2 stage twiddles, 4 stage-0 loads
 #endif
@@ -93,6 +96,14 @@ template <int L, int B> struct SmemGeom {
   static constexpr bool pp = LATTDSE_PINGPONG && tile * 16 <= 48 * 1024;
   static constexpr int bytes = (pp ? 2 : 1) * tile * 16;
 };
+
+LD_HD double2 __ldg_d2(const double2* p) {
+#if defined(__CUDA_ARCH__)
+  return __ldg(p);
+#else
+  return *p;
+#endif
+}
 
 template <int AXIS, int L, int B, int PROG> struct Ctx {
   double2* sm;   // buffer 0 (buffer 1 follows at sm + SmemGeom::tile when ping-ponging)
@@ -171,6 +182,34 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
     if (PROG == PROG_STOREDIAG) v = apply_diag(v, j);
     a.out[bat * a.out_bstride + j] = v;
   }
+  // Coefficients of the mid diagonal for elements j + r*T, r < R (zero where
+  // masked), fetched as one batch of independent loads: issued before the
+  // stage's twiddles and butterflies, their latency overlaps that work
+  // instead of serialising one table load per element after it.
+  template <int R, int T> LD_HD void mid_fetch(int b, int j, double2 (&dg)[R]) const {
+    const bool lv = live(b);
+    const double2 zero = make_double2(0.0, 0.0);
+    if (LATTDSE_ABLATE & 1) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) dg[r] = (lv && pos(b, j + r * T) < a.nvalid_mid) ? make_double2(1.0, 0.0) : zero;
+    } else if (dgt) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        dg[r] = (lv && pos(b, j + r * T) < a.nvalid_mid) ? dgt[b * L + j + r * T] : zero;
+    } else if (a.diag_kind == DG_CPLX) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const long long jj = pos(b, j + r * T);
+        dg[r] = (lv && jj < a.nvalid_mid) ? __ldg_d2(a.diag + jj) : zero;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const long long jj = pos(b, j + r * T);
+        dg[r] = (lv && jj < a.nvalid_mid) ? apply_diag(make_double2(1.0, 0.0), jj) : zero;
+      }
+    }
+  }
   // the mid diagonal and its mask are indexed by array position
   LD_HD double2 mid(int b, int i, double2 v) const {
     long long j = pos(b, i);
@@ -181,13 +220,6 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
   }
 };
 
-LD_HD double2 __ldg_d2(const double2* p) {
-#if defined(__CUDA_ARCH__)
-  return __ldg(p);
-#else
-  return *p;
-#endif
-}
 
 // Powers w^r, 0 <= r < R, of a twiddle from correctly rounded bases
 // w, w^4, w^16: every power is at most three products deep.
@@ -353,6 +385,10 @@ template <int AXIS, int L, int B, int NT, int SIGN, int SRC, int DST, int Q> str
       if (TASKS % NT != 0 && q >= TASKS) break;
       int b, j;
       First::map(q, b, j);
+#if LATTDSE_MID_PREFETCH
+      double2 dg[R];
+      c.template mid_fetch<R, T>(b, j, dg);
+#endif
       if (Ns > 1) {
         const double2* tw = c.a.fft_tw + P1::tw_offset(S1) + j;
         Pow<R> pw;
@@ -367,8 +403,13 @@ template <int AXIS, int L, int B, int NT, int SIGN, int SRC, int DST, int Q> str
         });
       }
       DFT<R, SIGN>::run(v[t]);
+#if LATTDSE_MID_PREFETCH
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[t][r] = c_mul(v[t][r], dg[r]);
+#else
 #pragma unroll
       for (int r = 0; r < R; ++r) v[t][r] = c.mid(b, j + r * T, v[t][r]);
+#endif
       DFT<R, -SIGN>::run(v[t]);  // second transform, stage 0 (Ns = 1: no twiddle)
       // stage-0 outputs of the reversed plan: idxD = j*R, positions j*R + r
       if (DST == DST_GLOBAL && AXIS == AX_COL && c.a.post_tw) First::fourstep(c, b, j, v[t], false);
@@ -477,6 +518,12 @@ __device__ __forceinline__ void load_tile(const PassArgs& a, double2* buf, doubl
 template <int AXIS, int L, int B, int NT, int PROG, int SIGN1, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) fft_pass_kernel(const __grid_constant__ PassArgs a) {
   extern __shared__ double2 lattdse_smem[];
+  // programmatic dependent launch (solver.cu, LATTDSE_PDL): let the next pass
+  // be scheduled onto SMs this grid's tail frees, and wait for the previous
+  // pass's results before touching them (both are no-ops without the launch
+  // attribute)
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   Ctx<AXIS, L, B, PROG> c{lattdse_smem, a, (int)blockIdx.x * B, (long long)blockIdx.y};
   run_pass<DevExec, AXIS, L, B, NT, PROG, SIGN1>(c);
 }

@@ -44,7 +44,8 @@ template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
     // caps (small L1-resident spills) against occupancy for 5-10 warp CTAs
     // ROW: 3 CTAs/SM; COL (four-step twiddle math in the fused stages) keeps
     // more registers at 2 CTAs/SM
-    k.default_mb = G::NT > 320 ? 2 : (AXIS == lattdse_dev::AX_ROW ? 3 : 2);
+    // ROW lines of 4096 (radix-16 stages) spill heavily under the 3-CTA cap
+    k.default_mb = G::NT > 320 ? 2 : (AXIS == lattdse_dev::AX_ROW && L < 4096 ? 3 : 2);
   }
   if constexpr (LATTDSE_BUILD_V2 && PROG == lattdse_dev::PROG_DOUBLE && G::smem2 <= 227 * 1024) {
     k.fn2 = reinterpret_cast<const void*>(&lattdse_dev::fft_pass2_kernel<AXIS, L, G::B, G::NT, SIGN>);

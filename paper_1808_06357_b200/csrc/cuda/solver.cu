@@ -257,6 +257,9 @@ struct Solver::Impl {
   static constexpr int kGraphSteps = 32;
   std::map<std::pair<long long, long long>, cudaGraphExec_t> graphs;
   bool use_graphs = std::getenv("LATTDSE_NO_GRAPHS") == nullptr;
+  // programmatic dependent launch between consecutive passes (opt-in LATTDSE_PDL=1:
+  // measured neutral on C1/C3, +1% on C2; profiles/README.md)
+  bool use_pdl = std::getenv("LATTDSE_PDL") && std::atoi(std::getenv("LATTDSE_PDL")) != 0;
   void drop_graphs() {
     for (auto& [k, g] : graphs) cudaGraphExecDestroy(g);
     graphs.clear();
@@ -304,24 +307,36 @@ struct Solver::Impl {
     void* args[] = {&a};
     const bool persist_this = persist_bytes > 0 && prog == PROG_DOUBLE && a.diag_kind == DG_CPLX &&
                               ((axis == AX_ROW && (persist_mode & 1)) || (axis == AX_COL && (persist_mode & 2)));
-    if (persist_this) {
-      // keep the per-step diagonal table (K^ / V) L2-resident across steps:
-      // it is read once per step and would otherwise be evicted by the
-      // streaming work buffer (profiles/README.md, steady-state DRAM bytes)
+    const bool pdl_this = use_pdl && !v2;
+    if (persist_this || pdl_this) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = grid;
       cfg.blockDim = dim3(k->NT);
       cfg.dynamicSmemBytes = (size_t)smem;
       cfg.stream = stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-      attr[0].val.accessPolicyWindow.base_ptr = (void*)a.diag;
-      attr[0].val.accessPolicyWindow.num_bytes = std::min<size_t>(persist_window, (size_t)table_bytes(a));
-      attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaLaunchAttribute attr[2];
+      int na = 0;
+      if (persist_this) {
+        // keep the per-step diagonal table (K^ / V) L2-resident across steps:
+        // it is read once per step and would otherwise be evicted by the
+        // streaming work buffer (profiles/README.md, steady-state DRAM bytes)
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = (void*)a.diag;
+        attr[na].val.accessPolicyWindow.num_bytes = std::min<size_t>(persist_window, (size_t)table_bytes(a));
+        attr[na].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+      }
+      if (pdl_this) {
+        // the pass waits (griddepcontrol.wait) for its predecessor's results;
+        // its CTAs may be scheduled while the predecessor's tail drains
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+      }
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = na;
       LD_CK(cudaLaunchKernelExC(&cfg, fn, args));
     } else {
       LD_CK(cudaLaunchKernel(fn, grid, dim3(k->NT), args, (size_t)smem, stream));
