@@ -62,6 +62,10 @@ struct AntiAliasSet {
 
   /// cap_radius <= 0 selects SPEC's default 4*n^(1/d) + 16.
   static AntiAliasSet build(const Lattice& lat, bool with_vectors = true, double cap_radius = -1.0);
+  /// Norms only, built on CUDA device `device` (rank-1; csrc/cuda/aaset_dev.cu).
+  /// Same norm2 table as build(). A Solver given an AntiAliasSet whose norm2
+  /// is empty builds this table on its own device instead.
+  static AntiAliasSet build_norms_device(const Lattice& lat, int device = 0, double cap_radius = -1.0);
   /// Brute-force minimality check over ||h||_inf <= bound.
   bool verify_minimal(const Lattice& lat, int bound) const;
   /// FNV-1a over the norm table (u32 little endian), for golden fixtures.

@@ -28,8 +28,9 @@ struct SolverOptions {
   std::string method = "circulant";
   /// members stepped together while L2-resident; 0 = automatic.
   std::int64_t group = 0;
-  /// force the length-M view M1 x M2 (rank-1; 0 = automatic)
-  std::int64_t force_M1 = 0, force_M2 = 0;
+  /// force the length-M view M1 x M2 (rank-1; 0 = automatic); with
+  /// force_M2a > 0 the rows are split three-level as M2 = M2a x (M2 / M2a)
+  std::int64_t force_M1 = 0, force_M2 = 0, force_M2a = 0;
 };
 
 struct ProblemSpec {
@@ -48,6 +49,7 @@ struct TrajectoryRow {
 
 struct SolverInfo {
   std::int64_t n_total, batch, M, M1, M2;
+  std::int64_t M2a;  // three-level inner split of M2 (0: two-level)
   int rank;
   std::string method;
   double bytes_per_step;        // algorithmic HBM bytes per step (whole batch), see DESIGN.md

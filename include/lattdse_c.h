@@ -76,6 +76,11 @@ int lattdse_cbc_construct(int64_t n, int d_max, int64_t* z_out, double* wce_out)
  * cap_radius <= 0 selects SPEC's default 4 n^(1/d) + 16. */
 int lattdse_aaset_build(const lattdse_lattice* lat, double cap_radius, uint32_t* norm2_out, int16_t* h_out,
                         uint32_t* max_norm2);
+/* The same norm table built on CUDA device `device` (rank-1, N < 2^31;
+ * meet-in-the-middle shell walk, csrc/cuda/aaset_dev.cu). norm2_out may be
+ * NULL (then only *max_norm2 is reported). */
+int lattdse_aaset_norms_device(const lattdse_lattice* lat, int device, double cap_radius, uint32_t* norm2_out,
+                               uint32_t* max_norm2);
 
 /* ---- problem families (BASELINE.json configs; SPEC.md:313-317 slots) --- */
 typedef struct lattdse_problem {
@@ -99,6 +104,9 @@ typedef struct lattdse_solver_opts {
   int device;        /* CUDA device ordinal                                */
   int method;        /* rank-1: 0 circulant (default), 1 literal Bluestein */
   int64_t group;     /* members stepped together (0 = auto, L2-sized)      */
+  /* rank-1 transform view (0 = automatic): M = force_M1 x force_M2; with
+   * force_M2a > 0 each row splits three-level as force_M2a x (M2/force_M2a) */
+  int64_t force_M1, force_M2, force_M2a;
 } lattdse_solver_opts;
 
 typedef struct lattdse_solver_info {
@@ -106,6 +114,7 @@ typedef struct lattdse_solver_info {
   int rank, method;
   double bytes_per_step, bytes_per_pass_col, bytes_per_pass_row;
   int launches_per_step;
+  int64_t M2a;       /* three-level inner split of M2 (0: two-level) */
 } lattdse_solver_info;
 
 /* Builds the anti-aliasing norm table, potential samples and device state. */

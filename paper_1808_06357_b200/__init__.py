@@ -220,6 +220,15 @@ def aaset_build(lat: Lattice, with_vectors: bool = True, cap_radius: float = -1.
     return norm2, h, mx.value
 
 
+def aaset_norms_device(lat: Lattice, device: int = 0, cap_radius: float = -1.0):
+    """The anti-aliasing norm table built on the GPU (rank-1); returns (norm2[u32], max_norm2)."""
+    norm2 = np.zeros(lat.n_total(), np.uint32)
+    mx = C.c_uint32()
+    _ck(_lib.lattdse_aaset_norms_device(lat.handle, device, C.c_double(cap_radius), _ptr(norm2, C.c_uint32),
+                                        C.byref(mx)))
+    return norm2, mx.value
+
+
 def problem_draw(seed: int, dim: int, batch: int, c_lo: float, c_hi: float, p_max: int):
     a = np.zeros(dim)
     b = np.zeros(max(dim - 1, 1))
@@ -237,14 +246,15 @@ class _Problem(C.Structure):
 
 
 class _Opts(C.Structure):
-    _fields_ = [("device", C.c_int), ("method", C.c_int), ("group", C.c_int64)]
+    _fields_ = [("device", C.c_int), ("method", C.c_int), ("group", C.c_int64), ("force_M1", C.c_int64),
+                ("force_M2", C.c_int64), ("force_M2a", C.c_int64)]
 
 
 class _Info(C.Structure):
     _fields_ = [("n_total", C.c_int64), ("batch", C.c_int64), ("M", C.c_int64), ("M1", C.c_int64),
                 ("M2", C.c_int64), ("group", C.c_int64), ("rank", C.c_int), ("method", C.c_int),
                 ("bytes_per_step", C.c_double), ("bytes_per_pass_col", C.c_double),
-                ("bytes_per_pass_row", C.c_double), ("launches_per_step", C.c_int)]
+                ("bytes_per_pass_row", C.c_double), ("launches_per_step", C.c_int), ("M2a", C.c_int64)]
 
 
 METHODS = {"circulant": 0, "bluestein": 1}
@@ -255,7 +265,8 @@ class Solver:
     """Device Strang propagator over the C ABI."""
 
     def __init__(self, lat: Lattice, eps: float, a, b, c, p, sigma: float, *, method: str = "circulant",
-                 device: int = 0, group: int = 0, norm2=None):
+                 device: int = 0, group: int = 0, norm2=None, geometry=None):
+        """geometry: None (automatic), (M1, M2) or three-level (M1, M2a, M2b)."""
         self.lat = lat
         d = lat.dim()
         self._a = np.ascontiguousarray(a, np.float64)
@@ -266,7 +277,11 @@ class Solver:
         self.n = lat.n_total()
         prob = _Problem(eps, d, _ptr(self._a, C.c_double), _ptr(self._b, C.c_double), self.batch, sigma,
                         _ptr(self._c, C.c_double), _ptr(self._p, C.c_int))
-        opts = _Opts(device, METHODS[method], group)
+        g = tuple(geometry or ())
+        if g and len(g) not in (2, 3):
+            raise ValueError("geometry is (M1, M2) or (M1, M2a, M2b)")
+        f1, f2, fa = (g[0], g[1], 0) if len(g) == 2 else ((g[0], g[1] * g[2], g[1]) if g else (0, 0, 0))
+        opts = _Opts(device, METHODS[method], group, f1, f2, fa)
         h = C.c_void_p()
         if norm2 is None:
             _ck(_lib.lattdse_solver_create(lat.handle, C.byref(prob), C.byref(opts), C.byref(h)))

@@ -79,6 +79,10 @@ struct PassArgs {
   int ncols_g;
   int rb_w, rb_n;
   long long rb_stride;
+  // Three-level rank-1 layout: a COL pass inside the rows of the M1 x M2 view
+  // (each row an Ma x Mb matrix, one per batch index) needs the four-step
+  // twiddles of length M2 = M / M1: W_M2^t = W_M^(M1 t). 0 or 1: plain.
+  long long tw_mul;
 };
 
 // Shared-memory slots of one tile: B lines, each Plan<L>::phys-swizzled and
@@ -144,7 +148,6 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
     const long long mask = (1LL << a.tw_shift) - 1;
     return c_mul(a.tw_hi[t >> a.tw_shift], a.tw_lo[t & mask]);
   }
-  LD_HD long long tw_index(int b, int i) const { return (long long)(a.col_off + line0 + b) * i; }
   LD_HD double2 apply_diag(double2 v, long long j) const {
     switch (a.diag_kind) {
       case DG_CPLX: return c_mul(v, a.diag[j]);
@@ -277,7 +280,7 @@ struct Stage {
   // four-step twiddles W(col * (j + r*T)) = W(col*j) * W(col*T)^r for the
   // elements j + r*T a task touches in stage 0 / the last stage
   LD_HD static void fourstep(const C& c, int b, int j, double2 (&v)[R], bool conj) {
-    const long long col = c.a.col_off + c.line0 + b;
+    const long long col = (long long)(c.a.col_off + c.line0 + b) * (c.a.tw_mul > 1 ? c.a.tw_mul : 1);
     const double2 base = c.twid(col * j);
     Pow<R> pw;
     pw.init(c.twid(col * T), R > 4 ? c.twid(col * 4 * T) : make_double2(1.0, 0.0),

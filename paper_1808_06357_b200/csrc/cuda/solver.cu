@@ -30,6 +30,7 @@
 
 #include "fft_pass.cuh"
 #include "lattdse/solver.hpp"
+#include "aaset_dev.hpp"
 #include "pass_registry.hpp"
 
 using namespace lattdse_dev;
@@ -79,6 +80,8 @@ std::vector<int> pass_lengths(int axis) {
 
 // --------------------------------------------------------- aux kernels
 namespace {
+
+constexpr int kMaxDimDev = 64;  // device-sampled rank-1 problems: d <= 64
 
 __global__ void k_phase(const double* __restrict__ v, long long n, double coef, double2* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -156,6 +159,57 @@ __global__ void k_mul(const double2* __restrict__ a, const double2* __restrict__
     out[i] = c_mul(a[i], b[i]);
 }
 
+// ---- rank-1 problem sampling on the device (problems.cpp restated: the
+// numerators (kappa z_j) mod N are exact 64-bit integers; trigonometric
+// arguments are formed from them reduced mod N)
+struct R1Points {
+  long long N;
+  int d;
+  long long z[kMaxDimDev];
+};
+__device__ __forceinline__ long long r1_num(const R1Points& P, long long k, int j) {
+  return (long long)(((unsigned long long)k * (unsigned long long)P.z[j]) % (unsigned long long)P.N);
+}
+__device__ __forceinline__ double cos2pi_frac_dev(long long a, long long L) {
+  long long r = a % L;
+  if (r < 0) r += L;
+  return cospi(2.0 * (double)r / (double)L);
+}
+// v(x) = sum_j a_j (1 - cos 2 pi x_j) + sum_{j<d} b_j cos 2 pi (x_j - x_{j+1})  (problems.cpp eval_v)
+__global__ void k_sample_v(const R1Points P, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ out) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < P.N; k += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < P.d; ++j) acc += a[j] * (1.0 - cos2pi_frac_dev(r1_num(P, k, j), P.N));
+    for (int j = 0; j + 1 < P.d; ++j) acc += b[j] * cos2pi_frac_dev(r1_num(P, k, j) - r1_num(P, k, j + 1), P.N);
+    out[k] = acc;
+  }
+}
+// unnormalised g (problems.cpp eval_g_unnormalized)
+__global__ void k_sample_g(const R1Points P, const double* __restrict__ c, const int* __restrict__ p, double inv2s2,
+                           double2* __restrict__ out) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < P.N; k += (long long)gridDim.x * blockDim.x) {
+    double expo = 0.0;
+    long long phase = 0;
+    for (int j = 0; j < P.d; ++j) {
+      const long long nj = r1_num(P, k, j);
+      const double s = sinpi((double)nj / (double)P.N - c[j]);
+      expo -= s * s * inv2s2;
+      phase += (long long)p[j] * nj;
+    }
+    long long ph = phase % P.N;
+    if (ph < 0) ph += P.N;
+    double sn, cs;
+    sincospi(2.0 * (double)ph / (double)P.N, &sn, &cs);
+    const double amp = exp(expo);
+    out[k] = make_double2(amp * cs, amp * sn);
+  }
+}
+__global__ void k_scale(double2* __restrict__ x, long long n, double s) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    x[i] = make_double2(x[i].x * s, x[i].y * s);
+}
+
 // Per-block partial sums of w_i * |x_i|^2 (w from a real table, an index
 // table scaled, or 1), batch along blockIdx.y.
 __global__ void k_wsumsq(const double2* __restrict__ x, long long n, long long bstride, const double* __restrict__ w,
@@ -231,9 +285,14 @@ struct Solver::Impl {
 
   // transform geometry
   long long M = 0, M1 = 0, M2 = 0;  // work = M1 rows x M2 cols
+  // three-level (rank-1, M beyond one COL x ROW split): each length-M2 row is
+  // itself an Ma x Mb four-step (COL pass of length Ma inside the row, ROW
+  // pass of length Mb); three = false: the ROW pass covers M2 directly
+  bool three = false;
+  long long Ma = 0, Mb = 0;
   int tw_shift = 0;
   bool pfa = false;                 // Good-Thomas layout (rank-1), else four-step
-  long long forced_M1 = 0, forced_M2 = 0;
+  long long forced_M1 = 0, forced_M2 = 0, forced_M2a = 0;
 
   // device
   int device = 0;
@@ -244,7 +303,7 @@ struct Solver::Impl {
   DBuf<double2> V, Vh, Ventry, Vexit, kin_lut, kin_full, Vperm;
   DBuf<unsigned short> nidx_perm;  // Good-Thomas: norm index in position order (sentinel = zero phase)
   DBuf<double2> Khat, B1hat, B2hat, chirp, chirp_c, chirp_n;
-  DBuf<double2> tw_col, tw_row, tw_col2, tw_row2, tw_lo, tw_hi, scal;
+  DBuf<double2> tw_col, tw_row, tw_col2, tw_row2, tw_mid, tw_mid2, tw_lo, tw_hi, scal;
   DBuf<double> partial;
   DBuf<char> flush;
   bool bluestein_tables = false;
@@ -301,6 +360,15 @@ struct Solver::Impl {
           if (f) LD_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         }
         k->attr_set = true;
+      }
+      if (nbatch > 65535) {  // grid.y limit: launch in batch chunks (tables are per position, shared)
+        for (long long b0 = 0; b0 < nbatch; b0 += 65535) {
+          PassArgs c = a;
+          c.in = a.in + b0 * a.in_bstride;
+          c.out = a.out + b0 * a.out_bstride;
+          launch_pass(axis, L, prog, sign, c, nlines, std::min<long long>(65535, nbatch - b0));
+        }
+        return;
       }
       grid = dim3((unsigned)((nlines + k->B - 1) / k->B), (unsigned)nbatch);
     }
@@ -377,6 +445,7 @@ struct Solver::Impl {
     a.pM1 = (int)M1;
     a.pM2 = (int)M2;
     a.pM = M;
+    a.tw_mul = 1;
     return a;
   }
   static void set_diag(PassArgs& a, const double2* d) {
@@ -436,22 +505,52 @@ struct Solver::Impl {
     set_diag(a, diag);
     launch_pass(AX_COL, (int)M1, PROG_STOREDIAG, +1, a, M2, nb);
   }
-  void r1_row_mid(double2* w, const double2* table, long long nb) {
+  // ROW pass over the rows of the view: length M2 (two-level) or Mb (three-level)
+  void r1_row_pass(int prog, int sign, double2* w, const double2* table, long long nb) {
     PassArgs a = base_args(AX_ROW);
     a.in = w;
     a.out = w;
     a.in_bstride = a.out_bstride = M;
     a.nvalid_in = a.nvalid_mid = a.nvalid_out = M;
     set_diag(a, table);
-    launch_pass(AX_ROW, (int)M2, PROG_DOUBLE, -1, a, M1, nb);
+    const long long L = three ? Mb : M2;
+    launch_pass(AX_ROW, (int)L, prog, sign, a, M / L, nb);
   }
-  void r1_row_fwd(double2* w) {
-    PassArgs a = base_args(AX_ROW);
+  // three-level: COL pass of length Ma inside every row (an Ma x Mb matrix;
+  // batch index = member * M1 + row), with the row's own four-step twiddles
+  // W_M2^(ka*nb) = W_M^(M1*ka*nb)
+  PassArgs mid_args(double2* w) const {
+    PassArgs a = base_args(AX_COL);
+    a.fft_tw = tw_mid.p;
+    a.fft_tw2 = tw_mid2.p;
+    a.ncols = (int)Mb;
+    a.tw_mul = M1;
     a.in = w;
     a.out = w;
-    a.in_bstride = a.out_bstride = M;
-    a.nvalid_in = a.nvalid_mid = a.nvalid_out = M;
-    launch_pass(AX_ROW, (int)M2, PROG_LOADDIAG, -1, a, M1, 1);
+    a.in_bstride = a.out_bstride = M2;
+    a.nvalid_in = a.nvalid_mid = a.nvalid_out = M2;
+    return a;
+  }
+  void r1_mid_fwd(double2* w, long long nb) {  // FFT_Ma, then x W_M2^(ka*nb)
+    PassArgs a = mid_args(w);
+    a.post_tw = 1;
+    launch_pass(AX_COL, (int)Ma, PROG_LOADDIAG, -1, a, Mb, M1 * nb);
+  }
+  void r1_mid_inv(double2* w, long long nb) {  // x conj W_M2^(ka*nb), then IFFT_Ma
+    PassArgs a = mid_args(w);
+    a.pre_tw = 1;
+    launch_pass(AX_COL, (int)Ma, PROG_STOREDIAG, +1, a, Mb, M1 * nb);
+  }
+  // per row of the view: FFT_M2 . (x table) . IFFT_M2 (table in the layout
+  // r1_row_fwd produces)
+  void r1_row_mid(double2* w, const double2* table, long long nb) {
+    if (three) r1_mid_fwd(w, nb);
+    r1_row_pass(PROG_DOUBLE, -1, w, table, nb);
+    if (three) r1_mid_inv(w, nb);
+  }
+  void r1_row_fwd(double2* w) {
+    if (three) r1_mid_fwd(w, 1);
+    r1_row_pass(PROG_LOADDIAG, -1, w, nullptr, 1);
   }
   // ---- rank-2 passes (ROW length n2 over n1 rows; COL length n1 over n2 cols)
   void g_row(int prog, int sign, const double2* in, double2* out, const double2* diag, long long nb) {
@@ -475,6 +574,46 @@ struct Solver::Impl {
     launch_pass(AX_COL, (int)n1, prog, sign, a, n2, nb);
   }
 
+  // ---- rank-1 problem sampling on the device
+  R1Points r1_points() const {
+    R1Points P{};
+    P.N = N;
+    P.d = dim;
+    const auto steps = lat.numerator_steps();
+    for (int j = 0; j < dim; ++j) P.z[j] = steps[0][j];
+    return P;
+  }
+  template <class T> void upload_small(DBuf<T>& b, const std::vector<T>& h) {
+    b.alloc(std::max<size_t>(1, h.size()));
+    if (!h.empty()) LD_CK(cudaMemcpyAsync(b.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, stream));
+  }
+  void sample_v_dev() {
+    DBuf<double> da, db;
+    upload_small(da, prob.potential.a);
+    upload_small(db, prob.potential.b);
+    v.alloc(N);
+    k_sample_v<<<grid1d(N), 256, 0, stream>>>(r1_points(), da.p, db.p, v.p);
+    aux_done("k_sample_v");
+    LD_CK(cudaStreamSynchronize(stream));  // da/db are freed at scope exit
+  }
+  // normalised g of member m into samples (problems.cpp sample_g restated)
+  void sample_g_dev(long long m) {
+    problems::Initial& g = prob.initial[m];
+    DBuf<double> dc;
+    DBuf<int> dp;
+    upload_small(dc, g.c);
+    upload_small(dp, g.p);
+    double2* out = samples.p + m * N;
+    k_sample_g<<<grid1d(N), 256, 0, stream>>>(r1_points(), dc.p, dp.p, 1.0 / (2.0 * g.sigma * g.sigma), out);
+    aux_done("k_sample_g");
+    const double tot = reduce(out, N, 1, N, nullptr, nullptr, 0.0, nullptr)[0];
+    if (!(tot > 0)) raise(Errc::non_normalizable, "initial condition vanishes on the lattice");
+    g.C = 1.0 / std::sqrt(tot / (double)N);
+    k_scale<<<grid1d(N), 256, 0, stream>>>(out, N, g.C);
+    aux_done("k_scale");
+    LD_CK(cudaStreamSynchronize(stream));
+  }
+
   // ---- setup
   void choose_geometry() {
     if (rank == 2) {
@@ -486,6 +625,29 @@ struct Solver::Impl {
       return;
     }
     const long long need = 2 * N - 1;
+    auto have3 = [&](long long g1, long long ga, long long gb) {
+      return g1 > 0 && ga > 0 && gb > 0 && g1 <= 4096 && ga <= 4096 && gb <= 4096 &&
+             dev::find_pass_kernel(AX_COL, (int)g1, PROG_DOUBLE, -1) &&
+             dev::find_pass_kernel(AX_COL, (int)ga, PROG_LOADDIAG, -1) &&
+             dev::find_pass_kernel(AX_ROW, (int)gb, PROG_DOUBLE, -1);
+    };
+    auto set3 = [&](long long g1, long long ga, long long gb) {
+      three = true;
+      pfa = false;
+      M1 = g1;
+      Ma = ga;
+      Mb = gb;
+      M2 = ga * gb;
+      M = M1 * M2;
+    };
+    if (forced_M1 > 0 && forced_M2 > 0 && forced_M2a > 0) {
+      if (forced_M2 % forced_M2a != 0 || forced_M1 * forced_M2 < need || !have3(forced_M1, forced_M2a, forced_M2 / forced_M2a))
+        raise(Errc::unsupported, "forced three-level geometry " + std::to_string(forced_M1) + "x" +
+                                     std::to_string(forced_M2a) + "x" + std::to_string(forced_M2 / std::max<long long>(1, forced_M2a)) +
+                                     " is not compiled or too small for N=" + std::to_string(N));
+      set3(forced_M1, forced_M2a, forced_M2 / forced_M2a);
+      return;
+    }
     if (forced_M1 > 0 && forced_M2 > 0) {
       if (forced_M1 * forced_M2 < need || !dev::find_pass_kernel(AX_COL, (int)forced_M1, PROG_DOUBLE, -1) ||
           !dev::find_pass_kernel(AX_ROW, (int)forced_M2, PROG_DOUBLE, -1))
@@ -497,8 +659,13 @@ struct Solver::Impl {
       pfa = false;
       return;
     }
-    if (const char* g = std::getenv("LATTDSE_GEOM")) {  // "M1xM2" override (experiments)
-      long long g1 = 0, g2 = 0;
+    if (const char* g = std::getenv("LATTDSE_GEOM")) {  // "M1xM2" / "M1xMaxMb" override (experiments)
+      long long g1 = 0, ga = 0, gb = 0;
+      if (std::sscanf(g, "%lldx%lldx%lld", &g1, &ga, &gb) == 3 && g1 * ga * gb >= need && have3(g1, ga, gb)) {
+        set3(g1, ga, gb);
+        return;
+      }
+      long long g2 = 0;
       if (std::sscanf(g, "%lldx%lld", &g1, &g2) == 2 && g1 * g2 >= need && dev::find_pass_kernel(AX_COL, (int)g1, PROG_DOUBLE, -1) &&
           dev::find_pass_kernel(AX_ROW, (int)g2, PROG_DOUBLE, -1)) {
         M1 = g1;
@@ -537,7 +704,31 @@ struct Solver::Impl {
         const long long m = (long long)L1 * L2;
         if (m >= need && (mmin < 0 || m < mmin)) mmin = m;
       }
-    if (mmin < 0) raise(Errc::unsupported, "N=" + std::to_string(N) + " exceeds the single-level four-step range");
+    if (mmin < 0) {
+      // three-level: smallest M = L1 * La * Lb >= 2N-1 (within 0.5%), then the
+      // lowest estimated cost; the inner COL passes run twice per step as
+      // single transforms (~0.6 of a fused double pass each)
+      long long m3 = -1;
+      for (int L1 : dev::pass_lengths(AX_COL))
+        for (int La : dev::pass_lengths(AX_COL))
+          for (int Lb : dev::pass_lengths(AX_ROW)) {
+            const long long m = (long long)L1 * La * Lb;
+            if (m >= need && (m3 < 0 || m < m3) && have3(L1, La, Lb)) m3 = m;
+          }
+      if (m3 < 0) raise(Errc::unsupported, "N=" + std::to_string(N) + " exceeds the three-level four-step range");
+      long long c1 = 0, ca = 0, cb = 0;
+      double bc = 0;
+      for (int L1 : dev::pass_lengths(AX_COL))
+        for (int La : dev::pass_lengths(AX_COL))
+          for (int Lb : dev::pass_lengths(AX_ROW)) {
+            const long long m = (long long)L1 * La * Lb;
+            if (m < need || (double)m > 1.005 * (double)m3 || !have3(L1, La, Lb)) continue;
+            const double cost = (double)m * (col_cost(L1) + 1.2 * col_cost(La) + row_cost(Lb));
+            if (c1 == 0 || cost < bc) { c1 = L1; ca = La; cb = Lb; bc = cost; }
+          }
+      set3(c1, ca, cb);
+      return;
+    }
     long long best = -1, b1 = 0, b2 = 0, bestp = -1, p1 = 0, p2 = 0;
     double bcost = 0, pcost = 0;
     for (int L1 : dev::pass_lengths(AX_COL))
@@ -578,9 +769,13 @@ struct Solver::Impl {
       return t;
     };
     up(tw_col, stage_tw(AX_COL, M1, false));
-    up(tw_row, stage_tw(AX_ROW, M2, false));
+    up(tw_row, stage_tw(AX_ROW, three ? Mb : M2, false));
     up(tw_col2, stage_tw(AX_COL, M1, true));
-    up(tw_row2, stage_tw(AX_ROW, M2, true));
+    up(tw_row2, stage_tw(AX_ROW, three ? Mb : M2, true));
+    if (three) {
+      up(tw_mid, stage_tw(AX_COL, Ma, false));
+      up(tw_mid2, stage_tw(AX_COL, Ma, true));
+    }
     tw_shift = 0;
     while ((1LL << (2 * tw_shift)) < M) ++tw_shift;
     const long long nlo = 1LL << tw_shift, nhi = (M + nlo - 1) / nlo;
@@ -767,11 +962,11 @@ struct Solver::Impl {
               LD_CK(cudaStreamEndCapture(stream, &g));
               LD_CK(cudaGraphInstantiate(&ge, g, 0));
               cudaGraphDestroy(g);
-              launches -= 2 * kGraphSteps;  // counted per replay below
+              launches -= (three ? 4 : 2) * kGraphSteps;  // counted per replay below
             }
             for (long long c = 0; c < chunks; ++c) {
               LD_CK(cudaGraphLaunch(ge, stream));
-              launches += 2 * kGraphSteps;
+              launches += (three ? 4 : 2) * kGraphSteps;
             }
             k = chunks * kGraphSteps;
           }
@@ -829,7 +1024,9 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
     s.n1 = lat.moduli()[0];
     s.n2 = lat.moduli()[1];
   }
-  if (aa.n_total != s.N) raise(Errc::spec_mismatch, "anti-aliasing set does not match the lattice");
+  const bool norms_on_device = aa.norm2.empty();  // build the norm table on this device (rank-1)
+  if (norms_on_device && s.rank != 1) raise(Errc::unsupported, "device-built norm tables need a rank-1 lattice");
+  if (!norms_on_device && aa.n_total != s.N) raise(Errc::spec_mismatch, "anti-aliasing set does not match the lattice");
   if (aa.max_norm2 > 65534) raise(Errc::unsupported, "||h||^2 above 65535 does not fit the uint16 norm index");
   if (prob.initial.empty()) raise(Errc::invalid_argument, "problem needs at least one initial condition");
   if (!(prob.eps > 0)) raise(Errc::invalid_argument, "eps must be > 0");
@@ -841,10 +1038,11 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
   s.method = s.rank == 2 ? "grid" : opt.method;
   if (s.rank == 1 && s.method != "circulant" && s.method != "bluestein")
     raise(Errc::invalid_argument, "method must be 'circulant' or 'bluestein'");
-  s.max_norm2 = aa.max_norm2;
+  s.max_norm2 = aa.max_norm2;  // device-built tables: set below
   s.device = opt.device;
   s.forced_M1 = opt.force_M1;
   s.forced_M2 = opt.force_M2;
+  s.forced_M2a = opt.force_M2a;
   LD_CK(cudaSetDevice(s.device));
   LD_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
   LD_CK(cudaDeviceGetAttribute(&s.num_sms, cudaDevAttrMultiProcessorCount, s.device));
@@ -883,14 +1081,24 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
   s.samples.alloc((size_t)s.N * s.batch);
   LD_CK(cudaMemsetAsync(s.samples.p, 0, sizeof(double2) * s.N * s.batch, s.stream));
 
-  // potential values and the norm index (host setup -> device, once)
-  auto vv = problems::sample_v(lat, prob.potential);
-  s.v.alloc(s.N);
-  LD_CK(cudaMemcpyAsync(s.v.p, vv.data(), sizeof(double) * s.N, cudaMemcpyHostToDevice, s.stream));
-  std::vector<unsigned short> ni(s.N);
-  for (long long c = 0; c < s.N; ++c) ni[c] = (unsigned short)aa.norm2[c];
+  // potential values (rank-1: sampled on the device) and the norm index
+  std::vector<double> vv;
+  if (s.rank == 1 && s.dim <= kMaxDimDev) {
+    s.sample_v_dev();
+  } else {
+    vv = problems::sample_v(lat, prob.potential);
+    s.v.alloc(s.N);
+    LD_CK(cudaMemcpyAsync(s.v.p, vv.data(), sizeof(double) * s.N, cudaMemcpyHostToDevice, s.stream));
+  }
   s.nidx.alloc(s.N);
-  LD_CK(cudaMemcpyAsync(s.nidx.p, ni.data(), sizeof(unsigned short) * s.N, cudaMemcpyHostToDevice, s.stream));
+  std::vector<unsigned short> ni;
+  if (norms_on_device) {
+    s.max_norm2 = dev::aaset_norms_device(lat, s.nidx.p, s.stream);
+  } else {
+    ni.resize(s.N);
+    for (long long c = 0; c < s.N; ++c) ni[c] = (unsigned short)aa.norm2[c];
+    LD_CK(cudaMemcpyAsync(s.nidx.p, ni.data(), sizeof(unsigned short) * s.N, cudaMemcpyHostToDevice, s.stream));
+  }
   LD_CK(cudaStreamSynchronize(s.stream));
 }
 
@@ -920,6 +1128,10 @@ void Solver::discretize_initial() {
   Impl& s = *p_;
   LD_CK(cudaSetDevice(s.device));
   for (long long m = 0; m < s.batch; ++m) {
+    if (s.rank == 1 && s.dim <= kMaxDimDev) {
+      s.sample_g_dev(m);
+      continue;
+    }
     problems::Initial g = s.prob.initial[m];
     auto gv = problems::sample_g(s.lat, g);
     LD_CK(cudaMemcpy(s.samples.p + m * s.N, gv.data(), sizeof(double2) * s.N, cudaMemcpyHostToDevice));
@@ -1088,6 +1300,7 @@ SolverInfo Solver::info() const {
   i.M = s.M;
   i.M1 = s.M1;
   i.M2 = s.M2;
+  i.M2a = s.three ? s.Ma : 0;
   i.rank = s.rank;
   i.method = s.method + (s.rank == 1 ? (s.pfa ? "/good-thomas" : "/four-step") : "");
   i.group = s.group;
@@ -1102,9 +1315,11 @@ SolverInfo Solver::info() const {
     // state R+W + V: four-step reads the N valid V entries, Good-Thomas the
     // position-ordered V_perm (M entries, mask folded in)
     i.bytes_per_pass_col = B * (32.0 * M + 16.0 * (s.pfa ? M : N));
-    i.bytes_per_pass_row = B * 32.0 * M + groups * 16.0 * M;  // state R+W + K^ once per group
+    // state R+W + K^ once per group; three-level: the "row" side is three
+    // passes (inner COL forward, ROW with K^, inner COL inverse)
+    i.bytes_per_pass_row = (s.three ? 3.0 : 1.0) * B * 32.0 * M + groups * 16.0 * M;
     i.bytes_per_step = i.bytes_per_pass_col + i.bytes_per_pass_row;
-    i.launches_per_step = 2 * (int)groups;
+    i.launches_per_step = (s.three ? 4 : 2) * (int)groups;
   } else {
     const double G = (double)s.group, groups = std::ceil(B / G);
     i.bytes_per_pass_col = B * (32.0 * M + 9.0 * N);   // avg of (V 16N) and (D idx 2N)

@@ -81,6 +81,9 @@ lattdse::SolverOptions make_opts(const lattdse_solver_opts* o) {
     so.device = o->device;
     so.method = o->method == 1 ? "bluestein" : "circulant";
     so.group = o->group;
+    so.force_M1 = o->force_M1;
+    so.force_M2 = o->force_M2;
+    so.force_M2a = o->force_M2a;
   }
   return so;
 }
@@ -258,6 +261,16 @@ int lattdse_aaset_build(const lattdse_lattice* lat, double cap_radius, uint32_t*
   });
 }
 
+int lattdse_aaset_norms_device(const lattdse_lattice* lat, int device, double cap_radius, uint32_t* norm2_out,
+                               uint32_t* max_norm2) {
+  return guard([&] {
+    need(lat, "lattice");
+    auto aa = lattdse::AntiAliasSet::build_norms_device(lat->lat, device, cap_radius);
+    if (norm2_out) std::copy(aa.norm2.begin(), aa.norm2.end(), norm2_out);
+    if (max_norm2) *max_norm2 = aa.max_norm2;
+  });
+}
+
 int lattdse_problem_draw(uint64_t seed, int dim, int64_t batch, double c_lo, double c_hi, int p_max, double* a,
                          double* b, double* c, int* p) {
   return guard([&] {
@@ -286,7 +299,10 @@ int lattdse_solver_create(const lattdse_lattice* lat, const lattdse_problem* pro
     need(lat, "lattice");
     need(out, "out");
     auto ps = make_problem(prob);
-    auto aa = lattdse::AntiAliasSet::build(lat->lat, false);
+    // rank-1: the solver builds the norm table on its device (empty norm2);
+    // rank-2: the host shell walk
+    lattdse::AntiAliasSet aa;
+    if (lat->lat.rank() != 1) aa = lattdse::AntiAliasSet::build(lat->lat, false);
     auto* h = new lattdse_solver;
     h->batch = prob->batch;
     try {
@@ -476,6 +492,7 @@ int lattdse_solver_info_get(lattdse_solver* s, lattdse_solver_info* out) {
     out->bytes_per_pass_col = i.bytes_per_pass_col;
     out->bytes_per_pass_row = i.bytes_per_pass_row;
     out->launches_per_step = i.launches_per_step;
+    out->M2a = i.M2a;
   });
 }
 

@@ -238,3 +238,54 @@ def test_sharded_config1(world):
     S.step(4)
     assert rel(D.get_state(), S.get_state()[0]) <= 1e-12
     assert abs(D.l2_norm() - 1.0) <= TOL_NORM
+
+
+def make_geom(lat, a, b, c, p, sigma, eps, dt, geometry, method="circulant"):
+    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    gen, moduli = lat.generators()
+    orc = Oracle(gen, moduli, norm2, eps, a, b)
+    orc.set_dt(dt)
+    S = L.Solver(lat, eps, a, b, c[:1], p[:1], sigma, method=method, norm2=norm2, geometry=geometry)
+    S.set_dt(dt)
+    S.discretize_initial()
+    return S, orc
+
+
+@pytest.mark.parametrize("method", ["circulant", "bluestein"])
+@pytest.mark.parametrize("geom", [(16, 24, 27), (9, 32, 32), (27, 9, 48)])
+def test_three_level_forced(geom, method):
+    """Three-level rank-1 layout (M = M1 x Ma x Mb: COL pass, then a COL pass
+    inside every row and a ROW pass) forced at a small N against the oracle."""
+    lat, a, b, c, p = configs.small_rank1(2, 4099, seed=31)
+    eps, dt, sigma = 0.1, 1.0 / 64, 0.1
+    S, orc = make_geom(lat, a, b, c, p, sigma, eps, dt, geom, method)
+    info = S.info()
+    assert (info["M1"], info["M2a"], info["M2"]) == (geom[0], geom[1], geom[1] * geom[2])
+    g, u0, u1 = oracle_coeffs(orc, c[0], p[0], sigma, 1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u0) <= 1e-13
+    S.step(1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u1) <= TOL_ONE
+    u10 = orc.steps(u1, 9)
+    S.step(9)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u10) <= TOL_RUN
+    assert abs(S.l2_norm()[0] - orc.l2_norm(u10)) <= TOL_NORM
+
+
+def test_three_level_automatic_beyond_two_level_range():
+    """N = smallest prime >= 2^23: 2N-1 exceeds 4096 x 4096, so the solver
+    must pick a three-level view on its own."""
+    n = 8388617
+    # z = cbc_construct(n, 3) (78 s on 8 host cores, so fixed here)
+    lat = L.Lattice.rank1([1, 2480387, 663367], n)
+    a, b, c, p = L.problem_draw(41, 3, 1, 0.4, 0.6, 2)
+    eps, dt, sigma = 0.05, 1.0 / 128, 0.1
+    S, orc = make_geom(lat, a, b, c, p, sigma, eps, dt, None)
+    info = S.info()
+    assert info["M2a"] > 0 and info["M"] >= 2 * n - 1
+    g, u0, u1 = oracle_coeffs(orc, c[0], p[0], sigma, 1)
+    S.step(1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u1) <= TOL_ONE
+    u4 = orc.steps(u1, 3)
+    S.step(3)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u4) <= TOL_RUN
+    assert abs(S.l2_norm()[0] - 1.0) <= TOL_NORM

@@ -1,0 +1,43 @@
+"""Device-side setup: the anti-aliasing norm table built on
+the GPU must equal the host shell walk's bit for bit, and a Solver that
+builds its own norm table on the device must step identically to one given
+the host table. (Potential / initial-condition sampling on the device is
+covered by every parity test: discretised samples vs the oracle.)"""
+import numpy as np
+import pytest
+
+import paper_1808_06357_b200 as L
+from paper_1808_06357_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("d,n", [(1, 8), (2, 55), (2, 4099), (3, 101), (4, 16411), (6, 65537)])
+def test_device_norms_small(d, n):
+    lat, *_ = configs.small_rank1(d, n, seed=5)
+    want, _, mx = L.aaset_build(lat, with_vectors=False)
+    got, gmx = L.aaset_norms_device(lat)
+    assert np.array_equal(got, want) and gmx == mx
+
+
+@pytest.mark.parametrize("name", ["C0", "C1", "C3"])
+def test_device_norms_configs(name):
+    lat = configs.lattice(configs.CONFIGS[name])
+    want, _, mx = L.aaset_build(lat, with_vectors=False)
+    got, gmx = L.aaset_norms_device(lat)
+    assert np.array_equal(got, want) and gmx == mx
+
+
+def test_solver_with_device_norms_matches_host_norms():
+    cfg = configs.CONFIGS["C0"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    out = []
+    for nv in (norm2, None):
+        S = L.Solver(lat, cfg.eps, a, b, c, p, cfg.sigma, norm2=nv)
+        S.set_dt(cfg.dt)
+        S.discretize_initial()
+        S.step(16)
+        out.append(S.get_state())
+    assert np.array_equal(out[0], out[1])
