@@ -43,6 +43,14 @@ Result construct(i64 n, int d_max);
 
 constexpr double kTieRel = 1e-13;
 
+/// The same construction on CUDA device `device` for prime n (csrc/cuda/
+/// solver.cu): the length-(n-1) correlation runs through the solver's
+/// length-M four-step FFT (M >= 2n-1, zero-padded linear correlation), the
+/// shortlist is re-scored by a compensated device sum (host long-double
+/// total). For n where the host construction is out of reach (config 4:
+/// n ~ 2^30, d = 20); equal to construct() on the sizes tests/ compare.
+Result construct_device(i64 n, int d_max, int device = 0);
+
 /// Exact criterion of candidate c given the running products P (double) --
 /// sequential long double sum over k = 0..n-1.
 double score_naive(const std::vector<double>& P, i64 c, i64 n, const std::vector<double>& om);

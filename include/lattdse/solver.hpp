@@ -89,6 +89,10 @@ class Solver {
   std::vector<double> energy();    // per member
   /// ||u - ref|| for member m, ref in the given space.
   double l2_distance(const std::complex<double>* ref, Space space, std::int64_t member = 0);
+  /// ||u - g|| for member m against its discretised initial condition,
+  /// formed on the device (time-reversibility checks at sizes whose state
+  /// does not fit host memory comfortably, config 4).
+  double l2_distance_initial(std::int64_t member = 0);
 
   /// Device time (ms) of nsteps steps bracketed by events on the solver stream.
   double time_steps(std::int64_t nsteps);
@@ -110,6 +114,7 @@ class Solver {
  private:
   struct Impl;
   std::unique_ptr<Impl> p_;
+  friend cbc::Result cbc::construct_device(i64 n, int d_max, int device);  // uses Impl as an FFT engine
 };
 
 }  // namespace lattdse

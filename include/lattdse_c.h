@@ -70,6 +70,9 @@ int lattdse_lattice_point_index(const lattdse_lattice* lat, int64_t flat_index, 
 int lattdse_wce_squared(const int64_t* z, int dim, int64_t n, double* out);
 /* z_out[d_max], wce_out[d_max] (criterion after each component, may be NULL) */
 int lattdse_cbc_construct(int64_t n, int d_max, int64_t* z_out, double* wce_out);
+/* The same construction on CUDA device `device` (prime n > 64, n < 2^31):
+ * the shortlisting correlation runs through the solver's length-M FFT. */
+int lattdse_cbc_construct_device(int64_t n, int d_max, int device, int64_t* z_out, double* wce_out);
 
 /* ---- antialias -------------------------------------- */
 /* norm2_out[n_total] = ||h^(chi)||^2; h_out[n_total*dim] (int16) or NULL;
@@ -138,6 +141,8 @@ int lattdse_solver_l2_norm(lattdse_solver* s, double* out);
 int lattdse_solver_energy(lattdse_solver* s, double* out);
 /* ||u_member - ref|| with ref in `space` */
 int lattdse_solver_l2_distance(lattdse_solver* s, const double* c128, int space, int64_t member, double* out);
+/* ||u - g|| against the member's discretised initial condition (device-side) */
+int lattdse_solver_l2_distance_initial(lattdse_solver* s, int64_t member, double* out);
 /* propagate: rows (step, time, norm, energy) for `member`;
  * rows_out holds floor(m/record_every)+2 rows of 4 doubles; *nrows set. */
 int lattdse_solver_propagate(lattdse_solver* s, int64_t m, int64_t record_every, int64_t member, double* rows_out,

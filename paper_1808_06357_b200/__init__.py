@@ -220,6 +220,14 @@ def aaset_build(lat: Lattice, with_vectors: bool = True, cap_radius: float = -1.
     return norm2, h, mx.value
 
 
+def cbc_construct_device(n: int, d_max: int, device: int = 0):
+    """CBC on the GPU (prime n > 64): returns (z[int64], wce[float64]) like cbc_construct."""
+    z = np.zeros(d_max, np.int64)
+    w = np.zeros(d_max)
+    _ck(_lib.lattdse_cbc_construct_device(C.c_int64(n), d_max, device, _ptr(z, C.c_int64), _ptr(w, C.c_double)))
+    return z, w
+
+
 def aaset_norms_device(lat: Lattice, device: int = 0, cap_radius: float = -1.0):
     """The anti-aliasing norm table built on the GPU (rank-1); returns (norm2[u32], max_norm2)."""
     norm2 = np.zeros(lat.n_total(), np.uint32)
@@ -358,6 +366,11 @@ class Solver:
         r = np.ascontiguousarray(ref, np.complex128).reshape(-1)
         out = C.c_double()
         _ck(_lib.lattdse_solver_l2_distance(self._h, r.ctypes.data_as(dblp), space, C.c_int64(member), C.byref(out)))
+        return out.value
+
+    def l2_distance_initial(self, member: int = 0) -> float:
+        out = C.c_double()
+        _ck(_lib.lattdse_solver_l2_distance_initial(self._h, C.c_int64(member), C.byref(out)))
         return out.value
 
     def propagate(self, m: int, record_every: int, member: int = 0) -> np.ndarray:

@@ -76,6 +76,9 @@ CONFIGS = {
              gen=[[1, 1557, 1741, 1031, 0, 0, 0, 0], [0, 0, 0, 0, 363, 1705, 1349, 1667]]),
     "C3": _c("C3", 3, 6, 262147, 0.05, 0.5, 512, 0.1, batch=512, c_range=(0.3, 0.7), p_max=3),
     "C4": _c("C4", 4, 20, 1073741827, 0.02, 0.1, 64, 0.15),
+    # config 4's shape at reduced N: d = 20, N = smallest
+    # prime >= 2^24; oracle-checkable, and the three-level layout's test case
+    "C4r": _c("C4r", 5, 20, 16777259, 0.02, 0.1, 64, 0.15),
 }
 
 

