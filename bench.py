@@ -158,20 +158,41 @@ def cpu_port_rate(cfg, lat, norm2, a, b, c, p, steps_per_sample: int, samples: i
     return cfg.N * steps_per_sample / statistics.mean(times), times
 
 
+CPU_MAX_N = 1 << 25  # the CPU port is timed on configs up to this size
+
+
+def cpu_case(cfg):
+    """(config, lattice, norm table, a, b, c, p, note) the CPU port is timed on:
+    the workload itself, or -- config 4, whose single state is 17 GB and whose
+    CPU step takes minutes -- its reduced-N twin C4r (same d, eps, T, m,
+    sigma; N = 16777259), the rate being per lattice-point step either way."""
+    import paper_1808_06357_b200 as L
+    from paper_1808_06357_b200 import configs
+
+    note = ""
+    if cfg.N > CPU_MAX_N and "C4r" in configs.CONFIGS:
+        cfg = configs.CONFIGS["C4r"]
+        note = " (C4r: config 4's shape at N = 16777259; the full-N CPU step does not fit a bounded sample)"
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg, batch=1)
+    if cfg.rank == 1 and cfg.d > 8:
+        # d = 20: the host shell walk takes hours; the oracle's norm-table INPUT is
+        # built on the device (bit-identical to the host walk, tests/test_gpu_setup.py)
+        norm2, _ = L.aaset_norms_device(lat)
+    else:
+        norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    return cfg, lat, norm2, a, b, c, p, note
+
+
 def run_reference(args, cfg):
     world, rank, _, dist, torch = dist_setup(args.gpus)
     if rank != 0:
         return 0
-    import paper_1808_06357_b200 as L
-    from paper_1808_06357_b200 import configs
-
-    lat = configs.lattice(cfg)
-    a, b, c, p = configs.problem(cfg, batch=1)
-    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    ccfg, lat, norm2, a, b, c, p, note = cpu_case(cfg)
     sample = max(1, args.ref_sample_steps)
     for _ in range(args.warmup):
-        cpu_port_rate(cfg, lat, norm2, a, b, c, p, 1)
-    rate, times = cpu_port_rate(cfg, lat, norm2, a, b, c, p, sample, samples=args.steps)
+        cpu_port_rate(ccfg, lat, norm2, a, b, c, p, 1)
+    rate, times = cpu_port_rate(ccfg, lat, norm2, a, b, c, p, sample, samples=args.steps)
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
@@ -179,8 +200,8 @@ def run_reference(args, cfg):
         "scaling": "weak", "vs_baseline": None, "dtype": "c128 (complex fp64)", "data": "synthetic (seeded BASELINE families)",
         "config": config_dict(cfg, args, note=f"1 reference step = {sample} Strang steps of the workload (bounded sample)"),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{sample} literal Strang steps of {cfg.name} per bench step (4 length-N DFTs each), "
-                                   f"OpenMP on {cores} host threads"},
+                         "sample": f"{sample} literal Strang steps of {ccfg.name} per bench step (4 length-N DFTs each), "
+                                   f"OpenMP on {cores} host threads{note}"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -218,7 +239,8 @@ def run_ours(args, cfg):
     else:
         batch = 1  # single wave function: every rank runs a replica
         members_all = world
-    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    # rank-1: the solver builds its norm table on the device (setup, untimed)
+    norm2 = None if cfg.rank == 1 else L.aaset_build(lat, with_vectors=False)[0]
     S = L.Solver(lat, cfg.eps, a, b, c, p, cfg.sigma, method=args.method, device=local, norm2=norm2)
     S.set_dt(cfg.dt)
     S.discretize_initial()
@@ -252,7 +274,9 @@ def run_ours(args, cfg):
     peak, peak_kind = measured_hbm_peak()
     dom = "col" if ms_col >= ms_row else "row"
     dom_ms = ms_col if dom == "col" else ms_row
-    dom_bytes = info["bytes_per_pass_col"] if dom == "col" else info["bytes_per_pass_row"]
+    # info's per-pass bytes cover the whole batch; one launch covers one group
+    groups = -(-batch // max(1, info["group"]))
+    dom_bytes = (info["bytes_per_pass_col"] if dom == "col" else info["bytes_per_pass_row"]) / groups
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -302,13 +326,13 @@ def run_ours(args, cfg):
     # ---- CPU baseline (rank 0, N=1 only): oracle port, bounded sample
     cpu = None
     if world == 1 and not args.no_cpu:
-        t0 = time.perf_counter()
-        rate1, _ = cpu_port_rate(cfg, lat, norm2, a, b, c, p, 1)
-        steps = max(1, min(64, int(args.cpu_seconds / max(cfg.N / rate1, 1e-3))))
-        rate, times = cpu_port_rate(cfg, lat, norm2, a, b, c, p, steps)
+        ccfg, clat, cnorm2, ca, cb, cc, cp, note = cpu_case(cfg)
+        rate1, _ = cpu_port_rate(ccfg, clat, cnorm2, ca, cb, cc, cp, 1)
+        steps = max(1, min(64, int(args.cpu_seconds / max(ccfg.N / rate1, 1e-3))))
+        rate, times = cpu_port_rate(ccfg, clat, cnorm2, ca, cb, cc, cp, steps)
         cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-               "sample": f"{steps} literal Strang steps of {cfg.name} (CPU oracle, OpenMP on {os.cpu_count()} threads), "
-                         f"{sum(times):.1f} s"}
+               "sample": f"{steps} literal Strang steps of {ccfg.name} (CPU oracle, OpenMP on {os.cpu_count()} threads), "
+                         f"{sum(times):.1f} s{note}"}
 
     if rank == 0:
         line = {

@@ -115,6 +115,19 @@ int main(int argc, char** argv) {
     run<AX_ROW, 1620, 1, 192, PROG_DOUBLE, -1, 3>(1296, 1620, 0, 0, -1, true);
     run<AX_COL, 1296, 2, 288, PROG_DOUBLE, 1, 2>(1296, 1620, 1, 1, -1, true);
     run<AX_COL, 1296, 2, 288, PROG_DOUBLE, 1, 2>(1296, 1620, 0, 0, -1, true);  // no four-step twiddles
+    if (argc > 2 && std::string(argv[2]) == "tpt") {  // two tasks per thread (ILP for TLP)
+      run<AX_ROW, 1620, 1, 96, PROG_DOUBLE, -1, 4>(1296, 1620, 0, 0, -1, true);
+      run<AX_ROW, 1620, 1, 96, PROG_DOUBLE, -1, 5>(1296, 1620, 0, 0, -1, true);
+      run<AX_ROW, 1620, 1, 128, PROG_DOUBLE, -1, 4>(1296, 1620, 0, 0, -1, true);
+      run<AX_ROW, 1620, 2, 192, PROG_DOUBLE, -1, 2>(1296, 1620, 0, 0, -1, true);
+      run<AX_ROW, 1620, 2, 384, PROG_DOUBLE, -1, 1>(1296, 1620, 0, 0, -1, true);
+      run<AX_COL, 1296, 2, 160, PROG_DOUBLE, 1, 3>(1296, 1620, 1, 1, -1, true);
+      run<AX_COL, 1296, 2, 160, PROG_DOUBLE, 1, 4>(1296, 1620, 1, 1, -1, true);
+      run<AX_COL, 1296, 2, 192, PROG_DOUBLE, 1, 3>(1296, 1620, 1, 1, -1, true);
+      run<AX_COL, 1296, 4, 288, PROG_DOUBLE, 1, 1>(1296, 1620, 1, 1, -1, true);
+      run<AX_COL, 1296, 4, 576, PROG_DOUBLE, 1, 1>(1296, 1620, 1, 1, -1, true);
+      run<AX_COL, 1296, 1, 160, PROG_DOUBLE, 1, 4>(1296, 1620, 1, 1, -1, true);
+    }
     return 0;
   }
   if (argc > 1) {
