@@ -115,6 +115,16 @@ int main(int argc, char** argv) {
     run<AX_ROW, 1620, 1, 192, PROG_DOUBLE, -1, 3>(1296, 1620, 0, 0, -1, true);
     run<AX_COL, 1296, 2, 288, PROG_DOUBLE, 1, 2>(1296, 1620, 1, 1, -1, true);
     run<AX_COL, 1296, 2, 288, PROG_DOUBLE, 1, 2>(1296, 1620, 0, 0, -1, true);  // no four-step twiddles
+    if (argc > 2 && std::string(argv[2]) == "c2") {  // config-2 column pass variants (4096 x 4096)
+      run<AX_COL, 4096, 1, 256, PROG_DOUBLE, -1, 2>(4096, 4096, 0, 0, -1, true);
+      run<AX_COL, 4096, 1, 256, PROG_DOUBLE, -1, 1>(4096, 4096, 0, 0, -1, true);
+      run<AX_COL, 4096, 2, 512, PROG_DOUBLE, -1, 1>(4096, 4096, 0, 0, -1, true);
+      run<AX_COL, 4096, 2, 256, PROG_DOUBLE, -1, 1>(4096, 4096, 0, 0, -1, true);
+      run<AX_ROW, 4096, 1, 256, PROG_DOUBLE, 1, 2>(4096, 4096, 0, 0, -1, true);
+      run<AX_COL, 64, 8, 128, PROG_DOUBLE, -1, 4>(64, 262144, 0, 0, -1, true);
+      run<AX_COL, 64, 16, 256, PROG_DOUBLE, -1, 3>(64, 262144, 0, 0, -1, true);
+      run<AX_COL, 64, 8, 128, PROG_LOADDIAG, -1, 4>(64, 262144, 1, 0, -1, true);
+    }
     if (argc > 2 && std::string(argv[2]) == "tpt") {  // two tasks per thread (ILP for TLP)
       run<AX_ROW, 1620, 1, 96, PROG_DOUBLE, -1, 4>(1296, 1620, 0, 0, -1, true);
       run<AX_ROW, 1620, 1, 96, PROG_DOUBLE, -1, 5>(1296, 1620, 0, 0, -1, true);

@@ -205,6 +205,17 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
         const long long jj = pos(b, j + r * T);
         dg[r] = (lv && jj < a.nvalid_mid) ? __ldg_d2(a.diag + jj) : zero;
       }
+    } else if (a.diag_kind == DG_LUT16) {
+      // norm index first (one batch), then the phase LUT (one batch)
+      const unsigned short* ix = (const unsigned short*)a.diag_idx;
+      unsigned short id[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const long long jj = pos(b, j + r * T);
+        id[r] = (lv && jj < a.nvalid_mid) ? ix[jj] : (unsigned short)0xFFFF;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) dg[r] = id[r] != 0xFFFF ? __ldg_d2(a.lut + id[r]) : zero;
     } else {
 #pragma unroll
       for (int r = 0; r < R; ++r) {

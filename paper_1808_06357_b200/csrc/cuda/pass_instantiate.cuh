@@ -8,7 +8,7 @@
 #define LATTDSE_BUILD_V2 0  // persistent double-buffered variant (opt-in, slower today)
 #endif
 #ifndef LATTDSE_COL_B1_MIN
-#define LATTDSE_COL_B1_MIN 4096  // columns this long: one column per CTA (smem for 3 CTAs/SM)
+#define LATTDSE_COL_B1_MIN 8192  // columns this long: one column per CTA
 #endif
 
 namespace lattdse::dev {
@@ -18,11 +18,15 @@ namespace lattdse::dev {
 //  COL lines are strided: B adjacent columns per CTA so every row segment a
 //  CTA touches is B*16 bytes (>= one 32-byte sector).
 // NT covers the busiest stage (B * L / R_min tasks) so no thread loops.
+//  COL lines of 4096 (config 2): two columns per CTA (32-byte row segments)
+//  at two tasks per thread, one CTA per SM with ~250 registers and no spills
+//  (measured 314 us vs 393 us for one column per CTA, profiles/README.md).
 template <int AXIS, int L> struct Geometry {
+  static constexpr bool wide_col = AXIS == lattdse_dev::AX_COL && L >= 4096 && L < LATTDSE_COL_B1_MIN;
   static constexpr int B = AXIS == lattdse_dev::AX_ROW ? (L >= 256 ? 1 : 256 / L)
                                                        : (L >= LATTDSE_COL_B1_MIN ? 1 : (L >= 512 ? 2 : (L >= 128 ? 4 : 8)));
   static constexpr int raw = B * lattdse_dev::Plan<L>::max_tasks();
-  static constexpr int NT = raw <= 32 ? 32 : (raw >= 512 ? 512 : ((raw + 31) / 32) * 32);
+  static constexpr int NT = wide_col ? 256 : (raw <= 32 ? 32 : (raw >= 512 ? 512 : ((raw + 31) / 32) * 32));
   static constexpr int smem2 = 2 * lattdse_dev::SmemGeom<L, B>::bytes + 2 * B * L * 16;  // v2 (opt-in)
 };
 
@@ -45,7 +49,7 @@ template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
     // ROW: 3 CTAs/SM; COL (four-step twiddle math in the fused stages) keeps
     // more registers at 2 CTAs/SM
     // ROW lines of 4096 (radix-16 stages) spill heavily under the 3-CTA cap
-    k.default_mb = G::NT > 320 ? 2 : (AXIS == lattdse_dev::AX_ROW && L < 4096 ? 3 : 2);
+    k.default_mb = G::wide_col ? 1 : (G::NT > 320 ? 2 : (AXIS == lattdse_dev::AX_ROW && L < 4096 ? 3 : 2));
   }
   if constexpr (LATTDSE_BUILD_V2 && PROG == lattdse_dev::PROG_DOUBLE && G::smem2 <= 227 * 1024) {
     k.fn2 = reinterpret_cast<const void*>(&lattdse_dev::fft_pass2_kernel<AXIS, L, G::B, G::NT, SIGN>);
