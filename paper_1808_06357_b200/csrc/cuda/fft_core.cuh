@@ -246,16 +246,22 @@ template <int SIGN> struct DFT<32, SIGN> : DFT_CT<4, 8, SIGN> {};
 // writes are bank-conflict free; otherwise (power-of-two-ish lengths) the
 // shared-memory layout is swizzled instead (Plan::swizzle).
 constexpr int kRadixPref[] = {16, 15, 12, 14, 9, 10, 8, 7, 6, 5, 4, 3, 2};
+// Largest radix for a line length: long lines whose fused middle stage would
+// hold two radix-16 tasks run register-lean radix-8 plans instead.
+#ifndef LATTDSE_MAXR_LONG
+#define LATTDSE_MAXR_LONG 16
+#endif
+constexpr int max_radix(int L) { return L >= 4096 ? LATTDSE_MAXR_LONG : 32; }
 
-constexpr int pick_radix(int rem) {
+constexpr int pick_radix(int rem, int maxr = 32) {
   for (int r : kRadixPref)
-    if (rem % r == 0) return r;
+    if (r <= maxr && rem % r == 0) return r;
   return rem;  // rejected by the static_assert in Plan
 }
 constexpr int first_radix(int L) {
   for (int r : {21, 15, 9})
-    if (L % r == 0) return r;
-  return pick_radix(L);
+    if (r <= max_radix(L) && L % r == 0) return r;
+  return pick_radix(L, max_radix(L));
 }
 
 template <int L> struct Plan {
@@ -264,7 +270,7 @@ template <int L> struct Plan {
     int r = first_radix(L);
     for (int i = 0; i < s; ++i) {
       rem /= r;
-      r = pick_radix(rem);
+      r = pick_radix(rem, max_radix(L));
     }
     return r;
   }
