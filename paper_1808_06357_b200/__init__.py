@@ -295,6 +295,9 @@ class Solver:
             _ck(_lib.lattdse_solver_create(lat.handle, C.byref(prob), C.byref(opts), C.byref(h)))
         else:
             nv = np.ascontiguousarray(norm2, np.uint32)
+            if nv.shape != (self.n,):
+                raise LattdseError(ERRC.index("spec_mismatch") + 1,
+                                   f"norm table has {nv.size} entries, the lattice {self.n} points")
             _ck(_lib.lattdse_solver_create_with_norms(lat.handle, _ptr(nv, C.c_uint32), C.byref(prob),
                                                       C.byref(opts), C.byref(h)))
         self._h = h
