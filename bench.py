@@ -292,7 +292,9 @@ def run_ours(args, cfg):
         "traffic": traffic, "kernel": f"{dom} pass (fft_pass_kernel, {'COL' if dom == 'col' else 'ROW'} axis)",
         "bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms, "peak_kind": peak_kind,
         "pass_ms": {"col": ms_col, "row": ms_row},
-        "note": "working set (~84 MB for C1) is L2-resident across steps; frac > 1 means L2 reuse, see DESIGN.md",
+        "note": (f"working set ~{info['bytes_per_step'] / 2 / 1e6:.0f} MB per pass: L2-resident across steps (126 MB L2); "
+                 "frac > 1 would mean L2 reuse, see DESIGN.md" if info["bytes_per_step"] / 2 < 100e6 else
+                 f"working set {info['bytes_per_step'] / 2 / 1e9:.1f} GB per pass streams through HBM"),
         "step_vs_canonical": {
             "canonical_bytes_per_step": canonical,
             "canonical_model": "160*M*+18*N (4 Bluestein passes, SURVEY.md 8(d))" if cfg.rank == 1 else "82*N",

@@ -880,6 +880,25 @@ struct Solver::Impl {
             if (m >= need && (m3 < 0 || m < m3) && have3(L1, La, Lb)) m3 = m;
           }
       if (m3 < 0) raise(Errc::unsupported, "N=" + std::to_string(N) + " exceeds the three-level four-step range");
+      // ps per element measured at config-4 size (tools/c4_geom_sweep.sh,
+      // profiles/README.md): first-level COL pass, and the row side (inner COL
+      // forward + ROW + inner COL inverse); unmeasured: the two-level tables
+      auto col3 = [&](int L) {
+        switch (L) {
+          case 1458: return 29.3; case 810: return 30.1; case 243: return 30.6; case 486: return 31.9;
+          case 1296: return 33.8; case 648: return 37.3; case 1620: return 38.8; case 720: return 38.9;
+          case 972: return 40.6; default: return 1.5 * col_cost(L);
+        }
+      };
+      auto row3 = [&](int La, int Lb) {
+        const long long k = (long long)La * 10000 + Lb;
+        switch (k) {
+          case 12962048: return 52.5; case 21602048: return 52.6; case 16202048: return 53.0;
+          case 16201024: return 55.0; case 12961024: return 55.8; case 12151215: return 56.3;
+          case 21604096: return 57.8; case 10802048: return 58.2; case 17281728: return 60.6;
+          default: return 1.5 * (1.2 * col_cost(La) + row_cost(Lb));
+        }
+      };
       long long c1 = 0, ca = 0, cb = 0;
       double bc = 0;
       for (int L1 : dev::pass_lengths(AX_COL))
@@ -887,7 +906,7 @@ struct Solver::Impl {
           for (int Lb : dev::pass_lengths(AX_ROW)) {
             const long long m = (long long)L1 * La * Lb;
             if (m < need || (double)m > 1.005 * (double)m3 || !have3(L1, La, Lb)) continue;
-            const double cost = (double)m * (col_cost(L1) + 1.2 * col_cost(La) + row_cost(Lb));
+            const double cost = (double)m * (col3(L1) + row3(La, Lb));
             if (c1 == 0 || cost < bc) { c1 = L1; ca = La; cb = Lb; bc = cost; }
           }
       set3(c1, ca, cb);
