@@ -363,7 +363,7 @@ def run_sharded(args, cfg):
 
     lat = configs.lattice(cfg)
     a, b, c, p = configs.problem(cfg, batch=1)
-    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    norm2 = None  # rank-1: the norm table is built on the device (bit-identical to the host walk)
     if world > 1:
         uid = [L.DistSolver.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -384,6 +384,16 @@ def run_sharded(args, cfg):
     total_ms = max_over_ranks(sum(per), dist, torch)
     norm = D.l2_norm()
     info = D.info()
+    # per-rank algorithmic bytes per Strang step: COL pass R+W
+    # of the column slab + V; row side R+W of the row slab per local pass
+    # (1, or 3 for three-level rows) + K^; exchanges: 2 per step, each rank
+    # sending (G-1) blocks of M/G^2 elements over NVLink
+    slab = info["M"] / G
+    row_passes = 3 if info.get("Ma", 0) else 1
+    hbm = 32.0 * slab + 16.0 * slab + row_passes * 32.0 * slab + 16.0 * slab
+    nvl = 2.0 * 16.0 * info["M"] * (G - 1) / (G * G)
+    t_roof = hbm / (measured_hbm_peak()[0] * 1e9) + (nvl / 900e9 if world > 1 else 0.0)
+    t_meas = 1e-3 * total_ms / (args.steps * m)
     if rank == 0:
         line = {
             "metric": METRIC, "value": float(cfg.N) * m * args.steps / (total_ms * 1e-3), "unit": UNIT,
@@ -394,6 +404,10 @@ def run_sharded(args, cfg):
                        f"({'NCCL send/recv' if world > 1 else 'virtual ranks on one GPU, device copies'}), "
                        "2 block exchanges per Strang step"},
             "sharded": {**info, "ranks": G, "norm_after": norm},
+            "roofline": {"bound": "hbm+nvlink", "hbm_bytes_per_rank_step": hbm, "nvlink_bytes_per_rank_step": nvl,
+                         "t_roof_us": 1e6 * t_roof, "frac": t_roof / t_meas,
+                         "note": "virtual ranks share one GPU's HBM: the exchange is device copies, not NVLink"
+                         if world == 1 else "HBM at MEASURED_PEAKS hbm_gbs, NVLink 900 GB/s per direction"},
             "us_per_strang_step": 1e3 * total_ms / (args.steps * m),
         }
         print(json.dumps(line), flush=True)

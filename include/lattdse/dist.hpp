@@ -5,6 +5,8 @@
 // exchanged block is contiguous on both sides). Between passes the ranks
 // exchange G x G blocks of (M1/G) x (M2/G) elements: two all-to-alls per
 // Strang step (the circulant step; the literal Bluestein step would need four).
+// Beyond one COL x ROW split (config 4) each row is itself an Ma x Mb
+// four-step handled locally on the row slab: still two exchanges per step.
 //
 // Exchange backends:
 //  - "local": all G ranks live on one device (virtual ranks); blocks move
@@ -50,6 +52,8 @@ class DistSolver {
   std::int64_t M() const;
   std::int64_t M1() const;
   std::int64_t M2() const;
+  /// three-level layout (M2 = Ma * Mb); 0 when the rows are one ROW pass
+  std::int64_t Ma() const;
   int world() const;
   /// bytes each rank sends per exchange (two exchanges per step)
   double exchange_bytes_per_rank() const;

@@ -174,7 +174,8 @@ int lattdse_solver_synchronize(lattdse_solver* s);
 /* ---- sharded single wave function (SURVEY.md §8(e), config 4 strategy) --
  * world ranks; rank = -1 runs all ranks as virtual ranks on `device` (block
  * exchanges by device copies), rank >= 0 is one process per GPU with NCCL
- * grouped send/recv (nccl_id from lattdse_dist_nccl_unique_id on rank 0). */
+ * grouped send/recv (nccl_id from lattdse_dist_nccl_unique_id on rank 0).
+ * norm2 = NULL: the norm table is built on the device (rank-1 lattices). */
 typedef struct lattdse_dist lattdse_dist;
 int lattdse_dist_nccl_unique_id(uint8_t* out128);
 int lattdse_dist_create(const lattdse_lattice* lat, const uint32_t* norm2, const lattdse_problem* prob, int world,
@@ -190,6 +191,8 @@ int lattdse_dist_l2_norm(lattdse_dist* d, double* out);
 int lattdse_dist_time_steps(lattdse_dist* d, int64_t nsteps, double* ms);
 /* M, M1, M2 of the sharded view; bytes each rank sends per exchange (2/step) */
 int lattdse_dist_info(lattdse_dist* d, int64_t* M, int64_t* M1, int64_t* M2, double* exchange_bytes);
+/* three-level row layout M2 = Ma x Mb of config-4-sized N (Ma = Mb = 0: two-level) */
+int lattdse_dist_three_level(lattdse_dist* d, int64_t* Ma, int64_t* Mb);
 
 #ifdef __cplusplus
 }

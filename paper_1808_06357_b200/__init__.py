@@ -476,7 +476,10 @@ class DistSolver:
         M, M1, M2 = C.c_int64(), C.c_int64(), C.c_int64()
         xb = C.c_double()
         _ck(_lib.lattdse_dist_info(self._h, C.byref(M), C.byref(M1), C.byref(M2), C.byref(xb)))
-        return {"M": M.value, "M1": M1.value, "M2": M2.value, "exchange_bytes_per_rank": xb.value}
+        Ma, Mb = C.c_int64(), C.c_int64()
+        _ck(_lib.lattdse_dist_three_level(self._h, C.byref(Ma), C.byref(Mb)))
+        return {"M": M.value, "M1": M1.value, "M2": M2.value, "Ma": Ma.value, "Mb": Mb.value,
+                "exchange_bytes_per_rank": xb.value}
 
 
 def snapshot_write(lat: Lattice, path: str, data, *, space: int = SAMPLES, step: int = 0, time: float = 0.0,

@@ -79,6 +79,10 @@ struct PassArgs {
   int ncols_g;
   int rb_w, rb_n;
   long long rb_stride;
+  // Three-level rows on a block-major row slab (each row an Ma x Mb matrix,
+  // Mb | rb_w): the single-transform COL passes of length Ma run inside the
+  // rows with batch = slab row, batch stride rb_w; the Mb-long ROW lines are
+  // contiguous, so the ROW pass sees the slab as plain lines (rb_w = 0).
   // Three-level rank-1 layout: a COL pass inside the rows of the M1 x M2 view
   // (each row an Ma x Mb matrix, one per batch index) needs the four-step
   // twiddles of length M2 = M / M1: W_M2^t = W_M^(M1 t). 0 or 1: plain.
@@ -129,6 +133,13 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
         return (long long)q * a.rb_stride + (long long)(line0 + b) * a.rb_w + (i - q * a.rb_w);
       }
       return (long long)(line0 + b) * L + i;
+    }
+    // inside a block-major slab row (the row is the batch index): single-
+    // transform programs only, so the fused per-step passes compile unchanged
+    if (PROG != PROG_DOUBLE && a.rb_w > 0) {
+      const int p = i * a.ncols + line0 + b;
+      const int q = p / a.rb_w;
+      return (long long)q * a.rb_stride + (p - q * a.rb_w);
     }
     return (long long)i * a.ncols + (line0 + b);
   }

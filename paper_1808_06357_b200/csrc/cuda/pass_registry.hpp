@@ -33,4 +33,11 @@ PassKernel* find_pass_kernel(int axis, int L, int prog, int sign);
 void register_pass_kernel(int axis, int L, int prog, int sign, const PassKernel& k);
 std::vector<int> pass_lengths(int axis);
 
+// measured pass costs, ps per element per pass (solver.cu): two-level COL /
+// ROW passes, three-level first-level COL pass and row side (La x Lb)
+double cost_col(int L);
+double cost_row(int L);
+double cost_col3(int L);
+double cost_row3(int La, int Lb);
+
 }  // namespace lattdse::dev

@@ -29,6 +29,7 @@
 #include <numeric>
 
 #include "fft_pass.cuh"
+#include "sampling.cuh"
 #include "lattdse/solver.hpp"
 #include "aaset_dev.hpp"
 #include "pass_registry.hpp"
@@ -81,7 +82,6 @@ std::vector<int> pass_lengths(int axis) {
 // --------------------------------------------------------- aux kernels
 namespace {
 
-constexpr int kMaxDimDev = 64;  // device-sampled rank-1 problems: d <= 64
 
 __global__ void k_phase(const double* __restrict__ v, long long n, double coef, double2* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -159,51 +159,17 @@ __global__ void k_mul(const double2* __restrict__ a, const double2* __restrict__
     out[i] = c_mul(a[i], b[i]);
 }
 
-// ---- rank-1 problem sampling on the device (problems.cpp restated: the
-// numerators (kappa z_j) mod N are exact 64-bit integers; trigonometric
-// arguments are formed from them reduced mod N)
-struct R1Points {
-  long long N;
-  int d;
-  long long z[kMaxDimDev];
-};
-__device__ __forceinline__ long long r1_num(const R1Points& P, long long k, int j) {
-  return (long long)(((unsigned long long)k * (unsigned long long)P.z[j]) % (unsigned long long)P.N);
-}
-__device__ __forceinline__ double cos2pi_frac_dev(long long a, long long L) {
-  long long r = a % L;
-  if (r < 0) r += L;
-  return cospi(2.0 * (double)r / (double)L);
-}
-// v(x) = sum_j a_j (1 - cos 2 pi x_j) + sum_{j<d} b_j cos 2 pi (x_j - x_{j+1})  (problems.cpp eval_v)
+// ---- rank-1 problem sampling on the device (sampling.cuh)
 __global__ void k_sample_v(const R1Points P, const double* __restrict__ a, const double* __restrict__ b,
                            double* __restrict__ out) {
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < P.N; k += (long long)gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int j = 0; j < P.d; ++j) acc += a[j] * (1.0 - cos2pi_frac_dev(r1_num(P, k, j), P.N));
-    for (int j = 0; j + 1 < P.d; ++j) acc += b[j] * cos2pi_frac_dev(r1_num(P, k, j) - r1_num(P, k, j + 1), P.N);
-    out[k] = acc;
-  }
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < P.N; k += (long long)gridDim.x * blockDim.x)
+    out[k] = sample_v_point(P, k, a, b);
 }
 // unnormalised g (problems.cpp eval_g_unnormalized)
 __global__ void k_sample_g(const R1Points P, const double* __restrict__ c, const int* __restrict__ p, double inv2s2,
                            double2* __restrict__ out) {
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < P.N; k += (long long)gridDim.x * blockDim.x) {
-    double expo = 0.0;
-    long long phase = 0;
-    for (int j = 0; j < P.d; ++j) {
-      const long long nj = r1_num(P, k, j);
-      const double s = sinpi((double)nj / (double)P.N - c[j]);
-      expo -= s * s * inv2s2;
-      phase += (long long)p[j] * nj;
-    }
-    long long ph = phase % P.N;
-    if (ph < 0) ph += P.N;
-    double sn, cs;
-    sincospi(2.0 * (double)ph / (double)P.N, &sn, &cs);
-    const double amp = exp(expo);
-    out[k] = make_double2(amp * cs, amp * sn);
-  }
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < P.N; k += (long long)gridDim.x * blockDim.x)
+    out[k] = sample_g_point(P, k, c, p, inv2s2);
 }
 __global__ void k_scale(double2* __restrict__ x, long long n, double s) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -419,6 +385,51 @@ std::vector<double2> root_table(long long n, long long count, long long stride) 
 }
 
 }  // namespace
+
+// ---- measured pass costs (ps per element per pass) for the geometry choice
+namespace dev {
+// C1 sweep (M = 2099520) where measured, else the C3 sweep (M = 524880, 8
+// members) scaled by 1.15 to C1's occupancy; unmeasured lengths get a
+// neutral estimate (profiles/README.md)
+double cost_col(int L) {
+  switch (L) {
+    case 486: return 19.4; case 729: return 21.4; case 1296: return 22.7; case 1215: return 22.7;
+    case 972: return 22.5; case 648: return 23.5; case 1458: return 25.4; case 810: return 25.5;
+    case 432: return 26.1; case 1944: return 26.4; case 1620: return 26.6; case 1728: return 27.5;
+    case 1080: return 27.6; case 540: return 31.4; case 405: return 33.9; case 720: return 37.3;
+    case 1440: return 38.8; default: return 30.0;
+  }
+}
+double cost_row(int L) {
+  switch (L) {
+    case 486: return 14.8; case 729: return 15.3; case 972: return 15.3; case 1620: return 16.7;
+    case 1296: return 18.0; case 648: return 18.2; case 1728: return 18.2; case 1215: return 18.8;
+    case 2160: return 18.8; case 1080: return 19.6; case 540: return 21.5; case 810: return 22.0;
+    case 720: return 22.1; case 1440: return 20.8; case 1458: return 22.7; case 1944: return 23.6;
+    case 405: return 24.8; case 432: return 25.0; default: return 22.0;
+  }
+}
+// measured at config-4 size (tools/c4_geom_sweep.sh, profiles/README.md):
+// first-level COL pass, and the row side (inner COL forward + ROW + inner
+// COL inverse); the inner COL passes run twice per step as single
+// transforms (~0.6 of a fused double pass each)
+double cost_col3(int L) {
+  switch (L) {
+    case 1458: return 29.3; case 810: return 30.1; case 243: return 30.6; case 486: return 31.9;
+    case 1296: return 33.8; case 648: return 37.3; case 1620: return 38.8; case 720: return 38.9;
+    case 972: return 40.6; default: return 1.5 * cost_col(L);
+  }
+}
+double cost_row3(int La, int Lb) {
+  const long long k = (long long)La * 10000 + Lb;
+  switch (k) {
+    case 12962048: return 52.5; case 21602048: return 52.6; case 16202048: return 53.0;
+    case 16201024: return 55.0; case 12961024: return 55.8; case 12151215: return 56.3;
+    case 21604096: return 57.8; case 10802048: return 58.2; case 17281728: return 60.6;
+    default: return 1.5 * (1.2 * cost_col(La) + cost_row(Lb));
+  }
+}
+}  // namespace dev
 
 // ------------------------------------------------------------- Impl
 struct Solver::Impl {
@@ -840,28 +851,9 @@ struct Solver::Impl {
       }
     }
     // Among the splits with the smallest M (within 0.5%), take the one with
-    // the lowest measured pass cost (ps per element, C1/C3 sweeps in
-    // profiles/README.md); unmeasured lengths get a neutral estimate.
-    // ps per element per pass; C1 sweep (M = 2099520) where measured, else
-    // the C3 sweep (M = 524880, 8 members) scaled by 1.15 to C1's occupancy
-    auto col_cost = [](int L) {
-      switch (L) {
-        case 486: return 19.4; case 729: return 21.4; case 1296: return 22.7; case 1215: return 22.7;
-        case 972: return 22.5; case 648: return 23.5; case 1458: return 25.4; case 810: return 25.5;
-        case 432: return 26.1; case 1944: return 26.4; case 1620: return 26.6; case 1728: return 27.5;
-        case 1080: return 27.6; case 540: return 31.4; case 405: return 33.9; case 720: return 37.3;
-        case 1440: return 38.8; default: return 30.0;
-      }
-    };
-    auto row_cost = [](int L) {
-      switch (L) {
-        case 486: return 14.8; case 729: return 15.3; case 972: return 15.3; case 1620: return 16.7;
-        case 1296: return 18.0; case 648: return 18.2; case 1728: return 18.2; case 1215: return 18.8;
-        case 2160: return 18.8; case 1080: return 19.6; case 540: return 21.5; case 810: return 22.0;
-        case 720: return 22.1; case 1440: return 20.8; case 1458: return 22.7; case 1944: return 23.6;
-        case 405: return 24.8; case 432: return 25.0; default: return 22.0;
-      }
-    };
+    // the lowest measured pass cost (dev::cost_* below)
+    auto col_cost = dev::cost_col;
+    auto row_cost = dev::cost_row;
     long long mmin = -1;
     for (int L1 : dev::pass_lengths(AX_COL))
       for (int L2 : dev::pass_lengths(AX_ROW)) {
@@ -880,25 +872,8 @@ struct Solver::Impl {
             if (m >= need && (m3 < 0 || m < m3) && have3(L1, La, Lb)) m3 = m;
           }
       if (m3 < 0) raise(Errc::unsupported, "N=" + std::to_string(N) + " exceeds the three-level four-step range");
-      // ps per element measured at config-4 size (tools/c4_geom_sweep.sh,
-      // profiles/README.md): first-level COL pass, and the row side (inner COL
-      // forward + ROW + inner COL inverse); unmeasured: the two-level tables
-      auto col3 = [&](int L) {
-        switch (L) {
-          case 1458: return 29.3; case 810: return 30.1; case 243: return 30.6; case 486: return 31.9;
-          case 1296: return 33.8; case 648: return 37.3; case 1620: return 38.8; case 720: return 38.9;
-          case 972: return 40.6; default: return 1.5 * col_cost(L);
-        }
-      };
-      auto row3 = [&](int La, int Lb) {
-        const long long k = (long long)La * 10000 + Lb;
-        switch (k) {
-          case 12962048: return 52.5; case 21602048: return 52.6; case 16202048: return 53.0;
-          case 16201024: return 55.0; case 12961024: return 55.8; case 12151215: return 56.3;
-          case 21604096: return 57.8; case 10802048: return 58.2; case 17281728: return 60.6;
-          default: return 1.5 * (1.2 * col_cost(La) + row_cost(Lb));
-        }
-      };
+      auto col3 = dev::cost_col3;
+      auto row3 = dev::cost_row3;
       long long c1 = 0, ca = 0, cb = 0;
       double bc = 0;
       for (int L1 : dev::pass_lengths(AX_COL))

@@ -10,6 +10,13 @@
 // Exchange col->row: A_g block h (rows of h, contiguous) -> B_h block g.
 // Exchange row->col: B_h block g -> A_g block h. Both sides contiguous, so
 // the NCCL path is G grouped send/recv pairs with no pack/unpack kernels.
+//
+// Three-level (config 4, M beyond one COL x ROW split): every length-M2 row
+// is an Ma x Mb matrix (M2 = Ma*Mb, G | Ma so each Mb-line lies inside one
+// Wb-wide block). The row side of a step is then three local passes on the
+// row slab -- COL pass of length Ma inside the rows (forward, four-step
+// twiddle W_M2), ROW pass of length Mb (x K^), COL pass inverse -- and the
+// step still needs exactly two exchanges.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -21,6 +28,7 @@
 #include <numeric>
 
 #include "fft_pass.cuh"
+#include "sampling.cuh"
 #include "lattdse/dist.hpp"
 #include "pass_registry.hpp"
 
@@ -109,6 +117,20 @@ __global__ void k_rowblk(const double2* __restrict__ src, long long M2, long lon
     out[p] = src[(row_off + r) * M2 + q * Wb + c];
   }
 }
+// unnormalised g on a column slab (zeros where the natural index >= N)
+__global__ void k_slab_sample_g(const R1Points P, const double* __restrict__ c, const int* __restrict__ pj, double inv2s2,
+                                long long M1, long long M2, long long Wb, long long col_off, double2* __restrict__ out) {
+  const long long n = M1 * Wb;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+    const long long j1 = q / Wb, cc = q - j1 * Wb;
+    const long long j = j1 * M2 + col_off + cc;
+    out[q] = j < P.N ? sample_g_point(P, j, c, pj, inv2s2) : make_double2(0.0, 0.0);
+  }
+}
+__global__ void k_scale_slab(double2* __restrict__ x, long long n, double s) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    x[i] = make_double2(x[i].x * s, x[i].y * s);
+}
 __global__ void k_sumsq(const double2* __restrict__ x, long long n, double* __restrict__ out) {
   __shared__ double red[32];
   double acc = 0.0;
@@ -160,16 +182,18 @@ std::vector<double2> roots(long long n, long long count, long long stride) {
 struct DistSolver::Impl {
   int G = 2, rank = -1, device = 0;
   long long N = 0, M = 0, M1 = 0, M2 = 0, Hb = 0, Wb = 0;
+  bool three = false;
+  long long Ma = 0, Mb = 0;  // three-level: M2 = Ma * Mb
   cudaStream_t stream = nullptr;
-  std::unique_ptr<Solver> full;  // builds the propagator tables (forced geometry)
   Lattice lat;
+  AntiAliasSet aa;               // empty norm2: built on the device by the table solver
   ProblemSpec prob;
   std::vector<int> local;        // ranks living in this process
   struct Rank {
     DBuf<double2> A, B, S, V, Vh, K;
   };
   std::vector<Rank> rk;          // indexed like `local`
-  DBuf<double2> tw_col, tw_row, tw_col2, tw_row2, tw_lo, tw_hi, tmp;
+  DBuf<double2> tw_col, tw_row, tw_col2, tw_row2, tw_mid, tw_mid2, tw_lo, tw_hi, tmp;
   DBuf<double> partial;
   int tw_shift = 0;
   ncclComm_t comm = nullptr;
@@ -178,8 +202,9 @@ struct DistSolver::Impl {
   explicit Impl(const Lattice& l) : lat(l) {}
 
   int grid1d(long long n) const { return (int)std::min<long long>((n + 255) / 256, 148 * 16); }
+  long long slab() const { return M1 * Wb; }
 
-  void launch(int axis, int L, int prog, int sign, PassArgs a, long long nlines) {
+  void launch(int axis, int L, int prog, int sign, PassArgs a, long long nlines, long long nbatch = 1) {
     dev::PassKernel* k = dev::find_pass_kernel(axis, L, prog, sign);
     if (!k) raise(Errc::unsupported, "no pass kernel for L=" + std::to_string(L));
     const void* fn = k->fn;
@@ -193,8 +218,8 @@ struct DistSolver::Impl {
     }
     a.nlines = (int)nlines;
     void* args[] = {&a};
-    LD_CK(cudaLaunchKernel(fn, dim3((unsigned)((nlines + k->B - 1) / k->B), 1), dim3(k->NT), args, (size_t)k->smem,
-                           stream));
+    LD_CK(cudaLaunchKernel(fn, dim3((unsigned)((nlines + k->B - 1) / k->B), (unsigned)nbatch), dim3(k->NT), args,
+                           (size_t)k->smem, stream));
   }
 
   PassArgs col_args(int g) const {
@@ -224,6 +249,25 @@ struct DistSolver::Impl {
     a.diag_kind = DG_CPLX;
     return a;
   }
+  // three-level: COL pass of length Ma inside each slab row (batch = row,
+  // batch stride Wb in the block-major slab), four-step twiddles of length
+  // M2: W_M2^t = W_M^(M1 t)
+  PassArgs mid_args() const {
+    PassArgs a{};
+    a.ncols = (int)Mb;
+    a.fft_tw = tw_mid.p;
+    a.fft_tw2 = tw_mid2.p;
+    a.tw_lo = tw_lo.p;
+    a.tw_hi = tw_hi.p;
+    a.tw_shift = tw_shift;
+    a.tw_mul = M1;
+    a.in_bstride = a.out_bstride = Wb;
+    a.nvalid_in = a.nvalid_mid = a.nvalid_out = Hb * M2;
+    a.rb_w = (int)Wb;
+    a.rb_n = G;
+    a.rb_stride = Hb * Wb;
+    return a;
+  }
 
   void upload_twiddles() {
     auto up = [&](DBuf<double2>& b, const std::vector<double2>& h) {
@@ -240,8 +284,12 @@ struct DistSolver::Impl {
     };
     up(tw_col, stage_tw(AX_COL, M1, false));
     up(tw_col2, stage_tw(AX_COL, M1, true));
-    up(tw_row, stage_tw(AX_ROW, M2, false));
-    up(tw_row2, stage_tw(AX_ROW, M2, true));
+    up(tw_row, stage_tw(AX_ROW, three ? Mb : M2, false));
+    up(tw_row2, stage_tw(AX_ROW, three ? Mb : M2, true));
+    if (three) {
+      up(tw_mid, stage_tw(AX_COL, Ma, false));
+      up(tw_mid2, stage_tw(AX_COL, Ma, true));
+    }
     tw_shift = 0;
     while ((1LL << (2 * tw_shift)) < M) ++tw_shift;
     const long long nlo = 1LL << tw_shift, nhi = (M + nlo - 1) / nlo;
@@ -249,25 +297,65 @@ struct DistSolver::Impl {
     up(tw_hi, roots(M, nhi, nlo));
   }
 
-  // choose M1 x M2 >= 2N-1 with G | M1, G | M2 among the compiled lengths
+  // M1 x M2 >= 2N-1 with G | M1, G | M2 among the compiled lengths (smallest
+  // M within 0.5%, then the lowest measured pass cost, as the unsharded
+  // solver chooses); beyond that range the three-level M1 x (Ma x Mb) with
+  // G | M1, G | Ma
   void choose_geometry() {
     const long long need = 2 * N - 1;
-    long long best = -1;
-    double bal = 0;
+    long long mmin = -1;
     for (int L1 : dev::pass_lengths(AX_COL))
       for (int L2 : dev::pass_lengths(AX_ROW)) {
         const long long m = (long long)L1 * L2;
-        if (m < need || L1 % G || L2 % G) continue;
-        const double bl = std::fabs(std::log((double)L1 / L2));
-        if (best < 0 || m < best || (m == best && bl < bal)) {
-          best = m;
-          bal = bl;
-          M1 = L1;
-          M2 = L2;
-        }
+        if (m >= need && L1 % G == 0 && L2 % G == 0 && (mmin < 0 || m < mmin)) mmin = m;
       }
-    if (best < 0) raise(Errc::unsupported, "no compiled M1 x M2 divisible by G=" + std::to_string(G));
-    M = best;
+    if (mmin > 0) {
+      double bc = 0;
+      for (int L1 : dev::pass_lengths(AX_COL))
+        for (int L2 : dev::pass_lengths(AX_ROW)) {
+          const long long m = (long long)L1 * L2;
+          if (m < need || L1 % G || L2 % G || (double)m > 1.005 * (double)mmin) continue;
+          const double cost = (double)m * (dev::cost_col(L1) + dev::cost_row(L2));
+          if (M == 0 || cost < bc) {
+            M = m;
+            M1 = L1;
+            M2 = L2;
+            bc = cost;
+          }
+        }
+      three = false;
+    } else {
+      auto have3 = [&](int L1, int La, int Lb) {
+        return L1 <= 4096 && La <= 4096 && Lb <= 4096 && L1 % G == 0 && La % G == 0 &&
+               dev::find_pass_kernel(AX_COL, L1, PROG_DOUBLE, -1) && dev::find_pass_kernel(AX_COL, La, PROG_LOADDIAG, -1) &&
+               dev::find_pass_kernel(AX_ROW, Lb, PROG_DOUBLE, -1);
+      };
+      long long m3 = -1;
+      for (int L1 : dev::pass_lengths(AX_COL))
+        for (int La : dev::pass_lengths(AX_COL))
+          for (int Lb : dev::pass_lengths(AX_ROW)) {
+            const long long m = (long long)L1 * La * Lb;
+            if (m >= need && (m3 < 0 || m < m3) && have3(L1, La, Lb)) m3 = m;
+          }
+      if (m3 < 0) raise(Errc::unsupported, "no compiled M1 x Ma x Mb >= 2N-1 with G=" + std::to_string(G) + " | M1, Ma");
+      double bc = 0;
+      for (int L1 : dev::pass_lengths(AX_COL))
+        for (int La : dev::pass_lengths(AX_COL))
+          for (int Lb : dev::pass_lengths(AX_ROW)) {
+            const long long m = (long long)L1 * La * Lb;
+            if (m < need || (double)m > 1.005 * (double)m3 || !have3(L1, La, Lb)) continue;
+            const double cost = (double)m * (dev::cost_col3(L1) + dev::cost_row3(La, Lb));
+            if (M == 0 || cost < bc) {
+              M = m;
+              M1 = L1;
+              Ma = La;
+              Mb = Lb;
+              bc = cost;
+            }
+          }
+      M2 = Ma * Mb;
+      three = true;
+    }
     Hb = M1 / G;
     Wb = M2 / G;
   }
@@ -334,11 +422,25 @@ struct DistSolver::Impl {
     a.pre_tw = 1;
     launch(AX_COL, (int)M1, PROG_STOREDIAG, +1, a, Wb);
   }
+  // the row side: FFT_M2 . (x K^) . IFFT_M2 on every row of the slab
   void row_mid(int i) {
+    if (three) {  // FFT_Ma inside the rows, then x W_M2^(ka*nb)
+      PassArgs a = mid_args();
+      a.in = a.out = rk[i].B.p;
+      a.post_tw = 1;
+      launch(AX_COL, (int)Ma, PROG_LOADDIAG, -1, a, Mb, Hb);
+    }
     PassArgs a = row_args();
     a.in = a.out = rk[i].B.p;
     a.diag = rk[i].K.p;
-    launch(AX_ROW, (int)M2, PROG_DOUBLE, -1, a, Hb);
+    if (three) a.rb_w = 0;  // slab = Hb*Ma contiguous Mb-lines (Mb | Wb); K^ sliced the same way
+    launch(AX_ROW, (int)(three ? Mb : M2), PROG_DOUBLE, -1, a, three ? Hb * Ma : Hb);
+    if (three) {  // x conj W_M2^(ka*nb), then IFFT_Ma
+      PassArgs b = mid_args();
+      b.in = b.out = rk[i].B.p;
+      b.pre_tw = 1;
+      launch(AX_COL, (int)Ma, PROG_STOREDIAG, +1, b, Mb, Hb);
+    }
   }
 
   void enqueue_steps(long long n) {
@@ -359,6 +461,27 @@ struct DistSolver::Impl {
     }
     LD_CK(cudaGetLastError());
   }
+
+  // sum over this process's slabs of sum |x|^2 (block partials, long double on the host)
+  double local_sumsq(const std::vector<const double2*>& xs) {
+    const int blocks = 592;
+    partial.alloc((size_t)blocks * xs.size() + 1);
+    for (size_t i = 0; i < xs.size(); ++i) k_sumsq<<<blocks, 256, 0, stream>>>(xs[i], slab(), partial.p + i * blocks);
+    std::vector<double> h((size_t)blocks * xs.size());
+    LD_CK(cudaMemcpyAsync(h.data(), partial.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    LD_CK(cudaStreamSynchronize(stream));
+    long double tot = 0;
+    for (double x : h) tot += x;
+    return (double)tot;
+  }
+  double allreduce_sum(double v) {
+    if (!comm) return v;
+    LD_CK(cudaMemcpyAsync(partial.p, &v, sizeof(double), cudaMemcpyHostToDevice, stream));
+    LD_NCCL(Nccl::get().AllReduce(partial.p, partial.p, 1, ncclDouble, ncclSum, comm, stream));
+    LD_CK(cudaMemcpyAsync(&v, partial.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    LD_CK(cudaStreamSynchronize(stream));
+    return v;
+  }
 };
 
 // --------------------------------------------------------------- DistSolver
@@ -369,36 +492,27 @@ DistSolver::DistSolver(const Lattice& lat, const AntiAliasSet& aa, const Problem
   if (prob.initial.size() != 1) raise(Errc::invalid_argument, "the sharded solver steps one wave function");
   if (opt.world < 1) raise(Errc::invalid_argument, "world must be >= 1");
   if (opt.rank >= opt.world) raise(Errc::invalid_argument, "rank must be < world");
+  if (!aa.norm2.empty() && aa.n_total != lat.n_total()) raise(Errc::spec_mismatch, "anti-aliasing set does not match the lattice");
   s.G = opt.world;
   s.rank = opt.rank;
   s.device = opt.device;
   s.N = lat.n_total();
+  s.aa = aa;
   s.prob = prob;
   LD_CK(cudaSetDevice(s.device));
   LD_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
   s.choose_geometry();
-  SolverOptions so;
-  so.device = s.device;
-  so.force_M1 = s.M1;
-  so.force_M2 = s.M2;
-  so.group = 1;
-  s.full = std::make_unique<Solver>(lat, aa, prob, so);
   s.upload_twiddles();
   if (s.rank < 0)
     for (int g = 0; g < s.G; ++g) s.local.push_back(g);
   else
     s.local.push_back(s.rank);
   s.rk.resize(s.local.size());
-  const size_t slab = (size_t)(s.M1 * s.Wb);
   for (auto& r : s.rk) {
-    r.A.alloc(slab);
-    r.B.alloc(slab);
-    r.S.alloc(slab);
-    r.V.alloc(slab);
-    r.Vh.alloc(slab);
-    r.K.alloc(slab);
-    LD_CK(cudaMemset(r.S.p, 0, slab * sizeof(double2)));
+    r.S.alloc((size_t)s.slab());
+    LD_CK(cudaMemsetAsync(r.S.p, 0, (size_t)s.slab() * sizeof(double2), s.stream));
   }
+  LD_CK(cudaStreamSynchronize(s.stream));
   if (s.rank >= 0 && s.G > 1) {
     if (!opt.nccl_id) raise(Errc::invalid_argument, "NCCL mode needs the rank-0 unique id");
     ncclUniqueId id;
@@ -420,21 +534,86 @@ void DistSolver::nccl_unique_id(void* out128) {
   std::memcpy(out128, &id, sizeof id);
 }
 
+// The propagator tables (K^ in ROW-pass order, V, V^(1/2)) come from an
+// unsharded Solver forced to this geometry, built for the call and freed
+// before the work slabs are allocated: each process holds the table solver
+// and its state slabs, then its slabs. When the slab tables do not fit next
+// to the table solver (config 4 at small G), they are staged through host
+// memory.
 void DistSolver::set_dt(double dt) {
   Impl& s = *p_;
   LD_CK(cudaSetDevice(s.device));
-  s.full->set_dt(dt);
-  const auto* K = (const double2*)s.full->device_table(0);
-  const auto* V = (const double2*)s.full->device_table(1);
-  const auto* Vh = (const double2*)s.full->device_table(2);
-  const long long slab = s.M1 * s.Wb;
-  for (size_t i = 0; i < s.local.size(); ++i) {
-    const int g = s.local[i];
-    k_colslab<<<s.grid1d(slab), 256, 0, s.stream>>>(V, s.N, s.M1, s.M2, s.Wb, g * s.Wb, s.rk[i].V.p);
-    k_colslab<<<s.grid1d(slab), 256, 0, s.stream>>>(Vh, s.N, s.M1, s.M2, s.Wb, g * s.Wb, s.rk[i].Vh.p);
-    k_rowblk<<<s.grid1d(slab), 256, 0, s.stream>>>(K, s.M2, s.Hb, s.Wb, s.G, g * s.Hb, s.rk[i].K.p);
+  s.have_dt = false;
+  for (auto& r : s.rk) {
+    r.A.release();
+    r.B.release();
+    r.V.release();
+    r.Vh.release();
+    r.K.release();
   }
-  LD_CK(cudaStreamSynchronize(s.stream));
+  const long long slab = s.slab();
+  const size_t sb = (size_t)slab * sizeof(double2);
+  std::vector<std::vector<double2>> host;  // staged [rank][table] when the slabs do not fit
+  {
+    SolverOptions so;
+    so.device = s.device;
+    so.force_M1 = s.M1;
+    so.force_M2 = s.M2;
+    so.force_M2a = s.three ? s.Ma : 0;
+    so.group = 1;
+    Solver full(s.lat, s.aa, s.prob, so);
+    full.set_dt(dt);
+    const auto* K = (const double2*)full.device_table(0);
+    const auto* V = (const double2*)full.device_table(1);
+    const auto* Vh = (const double2*)full.device_table(2);
+    size_t free_b = 0, total_b = 0;
+    LD_CK(cudaMemGetInfo(&free_b, &total_b));
+    const bool direct = (double)free_b > 3.0 * (double)sb * (double)s.local.size() + 2e9;
+    DBuf<double2> t;
+    if (!direct) {
+      t.alloc((size_t)slab);
+      host.assign(s.local.size(), std::vector<double2>((size_t)slab * 3));
+    }
+    for (size_t i = 0; i < s.local.size(); ++i) {
+      const int g = s.local[i];
+      auto& r = s.rk[i];
+      double2* dst[3];
+      if (direct) {
+        r.V.alloc((size_t)slab);
+        r.Vh.alloc((size_t)slab);
+        r.K.alloc((size_t)slab);
+        dst[0] = r.V.p;
+        dst[1] = r.Vh.p;
+        dst[2] = r.K.p;
+      } else {
+        dst[0] = dst[1] = dst[2] = t.p;
+      }
+      for (int w = 0; w < 3; ++w) {
+        if (w < 2)
+          k_colslab<<<s.grid1d(slab), 256, 0, s.stream>>>(w == 0 ? V : Vh, s.N, s.M1, s.M2, s.Wb, g * s.Wb, dst[w]);
+        else
+          k_rowblk<<<s.grid1d(slab), 256, 0, s.stream>>>(K, s.M2, s.Hb, s.Wb, s.G, g * s.Hb, dst[w]);
+        LD_CK(cudaGetLastError());
+        if (!direct)
+          LD_CK(cudaMemcpyAsync(host[i].data() + (size_t)w * slab, t.p, sb, cudaMemcpyDeviceToHost, s.stream));
+      }
+    }
+    LD_CK(cudaStreamSynchronize(s.stream));
+  }  // table solver and staging buffer freed
+  for (size_t i = 0; i < s.local.size(); ++i) {
+    auto& r = s.rk[i];
+    if (!host.empty()) {
+      r.V.alloc((size_t)slab);
+      r.Vh.alloc((size_t)slab);
+      r.K.alloc((size_t)slab);
+      LD_CK(cudaMemcpy(r.V.p, host[i].data(), sb, cudaMemcpyHostToDevice));
+      LD_CK(cudaMemcpy(r.Vh.p, host[i].data() + slab, sb, cudaMemcpyHostToDevice));
+      LD_CK(cudaMemcpy(r.K.p, host[i].data() + 2 * slab, sb, cudaMemcpyHostToDevice));
+      std::vector<double2>().swap(host[i]);
+    }
+    r.A.alloc((size_t)slab);
+    r.B.alloc((size_t)slab);
+  }
   LD_CK(cudaGetLastError());
   s.have_dt = true;
 }
@@ -444,17 +623,50 @@ void DistSolver::set_state(const std::complex<double>* samples) {
   LD_CK(cudaSetDevice(s.device));
   s.tmp.alloc(s.N);
   LD_CK(cudaMemcpyAsync(s.tmp.p, samples, s.N * sizeof(double2), cudaMemcpyHostToDevice, s.stream));
-  const long long slab = s.M1 * s.Wb;
+  const long long slab = s.slab();
   for (size_t i = 0; i < s.local.size(); ++i)
     k_colslab<<<s.grid1d(slab), 256, 0, s.stream>>>(s.tmp.p, s.N, s.M1, s.M2, s.Wb, s.local[i] * s.Wb, s.rk[i].S.p);
   LD_CK(cudaStreamSynchronize(s.stream));
+  s.tmp.release();
 }
 
+// g sampled on the device straight into the slabs (sampling.cuh, the same
+// point function as the unsharded solver), normalised by the all-rank sum
 void DistSolver::discretize_initial() {
   Impl& s = *p_;
-  problems::Initial g = s.prob.initial[0];
-  auto gv = problems::sample_g(s.lat, g);
-  set_state(gv.data());
+  LD_CK(cudaSetDevice(s.device));
+  problems::Initial& g = s.prob.initial[0];
+  const int d = s.lat.dim();
+  if (d > kMaxDimDev) {  // host sampling fallback for very high dimension
+    auto gv = problems::sample_g(s.lat, g);
+    set_state(gv.data());
+    return;
+  }
+  R1Points P{};
+  P.N = s.N;
+  P.d = d;
+  const auto steps = s.lat.numerator_steps();
+  for (int j = 0; j < d; ++j) P.z[j] = steps[0][j];
+  DBuf<double> dc;
+  DBuf<int> dp;
+  dc.alloc(d);
+  dp.alloc(d);
+  LD_CK(cudaMemcpy(dc.p, g.c.data(), d * sizeof(double), cudaMemcpyHostToDevice));
+  LD_CK(cudaMemcpy(dp.p, g.p.data(), d * sizeof(int), cudaMemcpyHostToDevice));
+  std::vector<const double2*> xs;
+  for (size_t i = 0; i < s.local.size(); ++i) {
+    k_slab_sample_g<<<s.grid1d(s.slab()), 256, 0, s.stream>>>(P, dc.p, dp.p, 1.0 / (2.0 * g.sigma * g.sigma), s.M1, s.M2,
+                                                              s.Wb, s.local[i] * s.Wb, s.rk[i].S.p);
+    LD_CK(cudaGetLastError());
+    xs.push_back(s.rk[i].S.p);
+  }
+  const double tot = s.allreduce_sum(s.local_sumsq(xs));
+  if (!(tot > 0)) raise(Errc::non_normalizable, "initial condition vanishes on the lattice");
+  const double C = 1.0 / std::sqrt(tot / (double)s.N);
+  g.C = C;
+  for (size_t i = 0; i < s.local.size(); ++i) k_scale_slab<<<s.grid1d(s.slab()), 256, 0, s.stream>>>(s.rk[i].S.p, s.slab(), C);
+  LD_CK(cudaStreamSynchronize(s.stream));
+  LD_CK(cudaGetLastError());
 }
 
 void DistSolver::get_state(std::complex<double>* samples) {
@@ -462,7 +674,7 @@ void DistSolver::get_state(std::complex<double>* samples) {
   LD_CK(cudaSetDevice(s.device));
   s.tmp.alloc(s.N);
   LD_CK(cudaMemcpyAsync(s.tmp.p, samples, s.N * sizeof(double2), cudaMemcpyHostToDevice, s.stream));
-  const long long slab = s.M1 * s.Wb;
+  const long long slab = s.slab();
   for (size_t i = 0; i < s.local.size(); ++i)
     k_slab2nat<<<s.grid1d(slab), 256, 0, s.stream>>>(s.rk[i].S.p, s.N, s.M1, s.M2, s.Wb, s.local[i] * s.Wb, s.tmp.p);
   LD_CK(cudaMemcpyAsync(samples, s.tmp.p, s.N * sizeof(double2), cudaMemcpyDeviceToHost, s.stream));
@@ -495,29 +707,15 @@ double DistSolver::time_steps(std::int64_t nsteps) {
 double DistSolver::l2_norm() {
   Impl& s = *p_;
   LD_CK(cudaSetDevice(s.device));
-  const long long slab = s.M1 * s.Wb;
-  const int blocks = 592;
-  s.partial.alloc((size_t)blocks * s.local.size() + 1);
-  for (size_t i = 0; i < s.local.size(); ++i)
-    k_sumsq<<<blocks, 256, 0, s.stream>>>(s.rk[i].S.p, slab, s.partial.p + i * blocks);
-  std::vector<double> h((size_t)blocks * s.local.size());
-  LD_CK(cudaMemcpyAsync(h.data(), s.partial.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
-  LD_CK(cudaStreamSynchronize(s.stream));
-  long double tot = 0;
-  for (double x : h) tot += x;
-  double sum = (double)tot;
-  if (s.comm) {
-    LD_CK(cudaMemcpyAsync(s.partial.p, &sum, sizeof(double), cudaMemcpyHostToDevice, s.stream));
-    LD_NCCL(Nccl::get().AllReduce(s.partial.p, s.partial.p, 1, ncclDouble, ncclSum, s.comm, s.stream));
-    LD_CK(cudaMemcpyAsync(&sum, s.partial.p, sizeof(double), cudaMemcpyDeviceToHost, s.stream));
-    LD_CK(cudaStreamSynchronize(s.stream));
-  }
-  return std::sqrt(sum / (double)s.N);
+  std::vector<const double2*> xs;
+  for (auto& r : s.rk) xs.push_back(r.S.p);
+  return std::sqrt(s.allreduce_sum(s.local_sumsq(xs)) / (double)s.N);
 }
 
 std::int64_t DistSolver::M() const { return p_->M; }
 std::int64_t DistSolver::M1() const { return p_->M1; }
 std::int64_t DistSolver::M2() const { return p_->M2; }
+std::int64_t DistSolver::Ma() const { return p_->three ? p_->Ma : 0; }
 int DistSolver::world() const { return p_->G; }
 double DistSolver::exchange_bytes_per_rank() const {
   return 16.0 * (double)p_->Hb * (double)p_->Wb * (double)(p_->G - 1);

@@ -564,9 +564,7 @@ int lattdse_dist_create(const lattdse_lattice* lat, const uint32_t* norm2, const
       aa.dim = lat->lat.dim();
       aa.norm2.assign(norm2, norm2 + aa.n_total);
       for (auto x : aa.norm2) aa.max_norm2 = std::max(aa.max_norm2, x);
-    } else {
-      aa = lattdse::AntiAliasSet::build(lat->lat, false);
-    }
+    }  // else: empty table -- the table-building solver builds the norms on its device (rank-1)
     lattdse::DistOptions o;
     o.world = world;
     o.rank = rank;
@@ -642,6 +640,16 @@ int lattdse_dist_info(lattdse_dist* d, int64_t* M, int64_t* M1, int64_t* M2, dou
     if (M1) *M1 = d->d->M1();
     if (M2) *M2 = d->d->M2();
     if (exchange_bytes) *exchange_bytes = d->d->exchange_bytes_per_rank();
+  });
+}
+
+int lattdse_dist_three_level(lattdse_dist* d, int64_t* Ma, int64_t* Mb) {
+  return guard([&] {
+    LD_NEED_D();
+    need(Ma, "Ma");
+    need(Mb, "Mb");
+    *Ma = d->d->Ma();
+    *Mb = *Ma > 0 ? d->d->M2() / *Ma : 0;
   });
 }
 

@@ -60,3 +60,38 @@ def test_config4_full_invariants():
     S.set_dt(-cfg.dt)
     S.step(cfg.m)
     assert S.l2_distance_initial() <= 1e-10
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_config4_reduced_sharded_virtual_ranks(world):
+    """Config 4's multi-GPU form: one wave function sharded
+    over `world` ranks with the three-level row side (M2 = Ma x Mb inside the
+    row slabs, two block exchanges per step), run as virtual ranks on one GPU
+    at C4r's N, against the oracle and the unsharded solver."""
+    cfg = configs.CONFIGS["C4r"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    norm2, _ = L.aaset_norms_device(lat)
+    gen, moduli = lat.generators()
+    orc = Oracle(gen, moduli, norm2, cfg.eps, a, b)
+    orc.set_dt(cfg.dt)
+    D = L.DistSolver(lat, cfg.eps, a, b, c, p, cfg.sigma, world=world, rank=-1)  # norms built on the device
+    info = D.info()
+    assert info["Ma"] > 0 and info["M"] >= 2 * cfg.N - 1
+    assert info["M1"] % world == 0 and info["Ma"] % world == 0
+    D.set_dt(cfg.dt)
+    D.discretize_initial()
+    g = orc.initial_samples(c[0], p[0], cfg.sigma)
+    assert rel(D.get_state(), g) <= 1e-13
+    assert abs(D.l2_norm() - 1.0) <= 1e-12
+    u1 = orc.steps(orc.analyze(g), 1)
+    D.step(1)
+    assert rel(orc.analyze(D.get_state()), u1) <= 1e-12
+    u3 = orc.steps(u1, 2)
+    D.step(2)
+    assert rel(orc.analyze(D.get_state()), u3) <= 1e-10
+    assert abs(D.l2_norm() - 1.0) <= 1e-12
+    # time reversibility through the sharded path
+    D.set_dt(-cfg.dt)
+    D.step(3)
+    assert rel(D.get_state(), g) <= 1e-10

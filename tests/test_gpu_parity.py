@@ -289,3 +289,30 @@ def test_three_level_automatic_beyond_two_level_range():
     S.step(3)
     assert rel(S.get_state(L.COEFFICIENTS)[0], u4) <= TOL_RUN
     assert abs(S.l2_norm()[0] - 1.0) <= TOL_NORM
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_sharded_three_level_automatic(world):
+    """N = 8388617: no two-level split covers 2N-1, so the sharded solver
+    runs three-level rows (Ma x Mb inside the row slabs) on its own; virtual
+    ranks vs the unsharded solver and the oracle."""
+    n = 8388617
+    lat = L.Lattice.rank1([1, 2480387, 663367], n)
+    a, b, c, p = L.problem_draw(41, 3, 1, 0.4, 0.6, 2)
+    eps, dt, sigma = 0.05, 1.0 / 128, 0.1
+    S, orc = make_geom(lat, a, b, c, p, sigma, eps, dt, None)
+    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    D = L.DistSolver(lat, eps, a, b, c, p, sigma, world=world, rank=-1, norm2=norm2)
+    info = D.info()
+    assert info["Ma"] > 0 and info["Ma"] * info["Mb"] == info["M2"]
+    assert info["M1"] % world == 0 and info["Ma"] % world == 0
+    D.set_dt(dt)
+    D.discretize_initial()
+    assert rel(D.get_state(), S.get_state()[0]) <= 1e-15
+    g, u0, u1 = oracle_coeffs(orc, c[0], p[0], sigma, 1)
+    D.step(1)
+    assert rel(orc.analyze(D.get_state()), u1) <= TOL_ONE
+    D.step(3)
+    S.step(4)
+    assert rel(D.get_state(), S.get_state()[0]) <= 1e-12
+    assert abs(D.l2_norm() - 1.0) <= TOL_NORM
