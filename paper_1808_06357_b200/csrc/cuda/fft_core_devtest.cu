@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "fft_pass.cuh"
+#include "pass_instantiate.cuh"
 
 using namespace lattdse_dev;
 
@@ -108,6 +109,13 @@ int run(long long nrows, long long ncols, int post_tw, int pre_tw, long long nin
   return e / mx < 1e-13 ? 0 : 1;
 }
 
+// production launch geometry of (AXIS, L) (pass_instantiate.cuh), PROG_DOUBLE
+template <int AXIS, int L> int time_prod(long long nrows, long long ncols, int tw) {
+  using G = lattdse::dev::Geometry<AXIS, L>;
+  constexpr int mb = G::wide_col ? 1 : (G::NT > 320 ? 2 : (AXIS == AX_ROW && L < 4096 ? 3 : 2));
+  return run<AXIS, L, G::B, G::NT, PROG_DOUBLE, AXIS == AX_ROW ? -1 : 1, mb>(nrows, ncols, tw, tw, -1, true);
+}
+
 int main(int argc, char** argv) {
   int bad = 0;
   if (argc > 1 && std::string(argv[1]) == "time") {
@@ -115,6 +123,25 @@ int main(int argc, char** argv) {
     run<AX_ROW, 1620, 1, 192, PROG_DOUBLE, -1, 3>(1296, 1620, 0, 0, -1, true);
     run<AX_COL, 1296, 2, 288, PROG_DOUBLE, 1, 2>(1296, 1620, 1, 1, -1, true);
     run<AX_COL, 1296, 2, 288, PROG_DOUBLE, 1, 2>(1296, 1620, 0, 0, -1, true);  // no four-step twiddles
+    if (argc > 2 && std::string(argv[2]) == "pow2") {  // power-of-two views of M = 2^21 (C1-sized)
+      time_prod<AX_ROW, 2048>(1024, 2048, 0);
+      time_prod<AX_COL, 1024>(1024, 2048, 1);
+      time_prod<AX_ROW, 1024>(2048, 1024, 0);
+      time_prod<AX_COL, 2048>(2048, 1024, 1);
+      time_prod<AX_ROW, 512>(4096, 512, 0);
+      time_prod<AX_COL, 4096>(4096, 512, 1);
+      time_prod<AX_ROW, 4096>(512, 4096, 0);
+      time_prod<AX_COL, 512>(512, 4096, 1);
+      time_prod<AX_ROW, 1620>(1296, 1620, 0);
+      time_prod<AX_COL, 1296>(1296, 1620, 1);
+      // column passes with a padded (non-power-of-two) row pitch
+      time_prod<AX_COL, 1024>(1024, 2064, 1);
+      time_prod<AX_COL, 1024>(1024, 2056, 1);
+      time_prod<AX_COL, 1024>(1024, 2050, 1);
+      time_prod<AX_COL, 2048>(2048, 1040, 1);
+      time_prod<AX_COL, 1024>(1024, 2064, 0);
+      time_prod<AX_COL, 1296>(1296, 1620, 0);
+    }
     if (argc > 2 && std::string(argv[2]) == "c2") {  // config-2 column pass variants (4096 x 4096)
       run<AX_COL, 4096, 1, 256, PROG_DOUBLE, -1, 2>(4096, 4096, 0, 0, -1, true);
       run<AX_COL, 4096, 1, 256, PROG_DOUBLE, -1, 1>(4096, 4096, 0, 0, -1, true);
