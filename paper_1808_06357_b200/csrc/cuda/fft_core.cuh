@@ -264,8 +264,28 @@ constexpr int first_radix(int L) {
   return pick_radix(L, max_radix(L));
 }
 
+// Explicit plans for long lines the greedy rule would end with a radix-2/3
+// stage (three balanced stages instead); {0} = use the greedy rule.
+struct PlanOverride {
+  int L, r[4];
+};
+constexpr PlanOverride kPlanOverride[] = {
+    {2592, {9, 16, 18, 0}},  {3240, {15, 12, 18, 0}}, {3888, {27, 16, 9, 0}},
+    {4320, {15, 16, 18, 0}}, {0, {0, 0, 0, 0}},
+};
+constexpr int override_radix(int L, int s) {
+  for (const auto& o : kPlanOverride)
+    if (o.L == L) return s < 4 ? o.r[s] : 0;
+  return -1;
+}
+
 template <int L> struct Plan {
   static constexpr int radix(int s) {
+    if (override_radix(L, 0) > 0) {
+      int rem = L;
+      for (int i = 0; i < s; ++i) rem /= override_radix(L, i);
+      return rem > 1 ? override_radix(L, s) : 1;
+    }
     int rem = L;
     int r = first_radix(L);
     for (int i = 0; i < s; ++i) {

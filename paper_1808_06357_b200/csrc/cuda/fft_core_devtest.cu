@@ -142,6 +142,37 @@ int main(int argc, char** argv) {
       time_prod<AX_COL, 1024>(1024, 2064, 0);
       time_prod<AX_COL, 1296>(1296, 1620, 0);
     }
+    if (argc > 2 && std::string(argv[2]) == "long") {  // C1's M = 2099520 with short columns, long rows
+      time_prod<AX_ROW, 2592>(810, 2592, 0);
+      time_prod<AX_COL, 810>(810, 2592, 1);
+      time_prod<AX_ROW, 2880>(729, 2880, 0);
+      time_prod<AX_COL, 729>(729, 2880, 1);
+      time_prod<AX_ROW, 3240>(648, 3240, 0);
+      time_prod<AX_COL, 648>(648, 3240, 1);
+      time_prod<AX_ROW, 3888>(540, 3888, 0);
+      time_prod<AX_COL, 540>(540, 3888, 1);
+      time_prod<AX_ROW, 4320>(486, 4320, 0);
+      time_prod<AX_COL, 486>(486, 4320, 1);
+      time_prod<AX_ROW, 2160>(972, 2160, 0);
+      time_prod<AX_COL, 972>(972, 2160, 1);
+    }
+    if (argc > 2 && std::string(argv[2]) == "longmb") {  // long rows at other register caps
+      using namespace lattdse::dev;
+      run<AX_ROW, 2592, 1, Geometry<AX_ROW, 2592>::NT, PROG_DOUBLE, -1, 1>(810, 2592, 0, 0, -1, true);
+      run<AX_ROW, 2592, 1, Geometry<AX_ROW, 2592>::NT, PROG_DOUBLE, -1, 2>(810, 2592, 0, 0, -1, true);
+      run<AX_ROW, 2880, 1, Geometry<AX_ROW, 2880>::NT, PROG_DOUBLE, -1, 1>(729, 2880, 0, 0, -1, true);
+      run<AX_ROW, 2880, 1, Geometry<AX_ROW, 2880>::NT, PROG_DOUBLE, -1, 2>(729, 2880, 0, 0, -1, true);
+      run<AX_ROW, 3240, 1, Geometry<AX_ROW, 3240>::NT, PROG_DOUBLE, -1, 1>(648, 3240, 0, 0, -1, true);
+      run<AX_ROW, 3240, 1, Geometry<AX_ROW, 3240>::NT, PROG_DOUBLE, -1, 2>(648, 3240, 0, 0, -1, true);
+      run<AX_ROW, 3888, 1, Geometry<AX_ROW, 3888>::NT, PROG_DOUBLE, -1, 1>(540, 3888, 0, 0, -1, true);
+      run<AX_ROW, 4320, 1, Geometry<AX_ROW, 4320>::NT, PROG_DOUBLE, -1, 1>(486, 4320, 0, 0, -1, true);
+      run<AX_ROW, 2160, 1, Geometry<AX_ROW, 2160>::NT, PROG_DOUBLE, -1, 2>(972, 2160, 0, 0, -1, true);
+      run<AX_ROW, 4096, 1, 256, PROG_DOUBLE, -1, 2>(512, 4096, 0, 0, -1, true);
+      run<AX_COL, 486, 4, Geometry<AX_COL, 486>::NT, PROG_DOUBLE, 1, 1>(486, 4320, 1, 1, -1, true);
+      run<AX_COL, 486, 4, Geometry<AX_COL, 486>::NT, PROG_DOUBLE, 1, 3>(486, 4320, 1, 1, -1, true);
+      run<AX_COL, 512, 4, 256, PROG_DOUBLE, 1, 2>(512, 4096, 1, 1, -1, true);
+      run<AX_COL, 512, 4, 256, PROG_DOUBLE, 1, 3>(512, 4096, 1, 1, -1, true);
+    }
     if (argc > 2 && std::string(argv[2]) == "c2") {  // config-2 column pass variants (4096 x 4096)
       run<AX_COL, 4096, 1, 256, PROG_DOUBLE, -1, 2>(4096, 4096, 0, 0, -1, true);
       run<AX_COL, 4096, 1, 256, PROG_DOUBLE, -1, 1>(4096, 4096, 0, 0, -1, true);

@@ -23,10 +23,14 @@ namespace lattdse::dev {
 //  (measured 314 us vs 393 us for one column per CTA, profiles/README.md).
 template <int AXIS, int L> struct Geometry {
   static constexpr bool wide_col = AXIS == lattdse_dev::AX_COL && L >= 4096 && L < LATTDSE_COL_B1_MIN;
+  // COL 512 (the power-of-two view 512 x 4096 of config 1): four columns
+  // (64-byte row segments) at 256 threads, measured 32.1 us vs 79 us for two
+  // columns at 512 threads (profiles/README.md)
+  static constexpr bool col512 = AXIS == lattdse_dev::AX_COL && L == 512;
   static constexpr int B = AXIS == lattdse_dev::AX_ROW ? (L >= 256 ? 1 : 256 / L)
-                                                       : (L >= LATTDSE_COL_B1_MIN ? 1 : (L >= 512 ? 2 : (L >= 128 ? 4 : 8)));
+                                                       : (L >= LATTDSE_COL_B1_MIN ? 1 : (L >= 512 && !col512 ? 2 : (L >= 128 ? 4 : 8)));
   static constexpr int raw = B * lattdse_dev::Plan<L>::max_tasks();
-  static constexpr int NT = wide_col ? 256 : (raw <= 32 ? 32 : (raw >= 512 ? 512 : ((raw + 31) / 32) * 32));
+  static constexpr int NT = (wide_col || col512) ? 256 : (raw <= 32 ? 32 : (raw >= 512 ? 512 : ((raw + 31) / 32) * 32));
   static constexpr int smem2 = 2 * lattdse_dev::SmemGeom<L, B>::bytes + 2 * B * L * 16;  // v2 (opt-in)
 };
 
