@@ -173,6 +173,19 @@ int main(int argc, char** argv) {
       run<AX_COL, 512, 4, 256, PROG_DOUBLE, 1, 2>(512, 4096, 1, 1, -1, true);
       run<AX_COL, 512, 4, 256, PROG_DOUBLE, 1, 3>(512, 4096, 1, 1, -1, true);
     }
+    if (argc > 2 && std::string(argv[2]) == "colb4") {  // four columns per CTA at C1-compatible geometries
+      run<AX_COL, 729, 4, 352, PROG_DOUBLE, 1, 1>(729, 2880, 1, 1, -1, true);
+      run<AX_COL, 729, 4, 352, PROG_DOUBLE, 1, 2>(729, 2880, 1, 1, -1, true);
+      run<AX_COL, 972, 4, 448, PROG_DOUBLE, 1, 1>(972, 2160, 1, 1, -1, true);
+      run<AX_COL, 972, 4, 448, PROG_DOUBLE, 1, 2>(972, 2160, 1, 1, -1, true);
+      run<AX_COL, 648, 4, 448, PROG_DOUBLE, 1, 1>(648, 3240, 1, 1, -1, true);
+      run<AX_COL, 648, 4, 448, PROG_DOUBLE, 1, 2>(648, 3240, 1, 1, -1, true);
+      run<AX_COL, 810, 4, 544, PROG_DOUBLE, 1, 1>(810, 2592, 1, 1, -1, true);
+      run<AX_COL, 1296, 4, 576, PROG_DOUBLE, 1, 1>(1296, 1620, 1, 1, -1, true);
+      run<AX_COL, 1215, 4, 544, PROG_DOUBLE, 1, 1>(1215, 1728, 1, 1, -1, true);
+      run<AX_ROW, 1728, 1, 224, PROG_DOUBLE, -1, 3>(1215, 1728, 0, 0, -1, true);
+      run<AX_COL, 1215, 2, 272, PROG_DOUBLE, 1, 2>(1215, 1728, 1, 1, -1, true);
+    }
     if (argc > 2 && std::string(argv[2]) == "c2") {  // config-2 column pass variants (4096 x 4096)
       run<AX_COL, 4096, 1, 256, PROG_DOUBLE, -1, 2>(4096, 4096, 0, 0, -1, true);
       run<AX_COL, 4096, 1, 256, PROG_DOUBLE, -1, 1>(4096, 4096, 0, 0, -1, true);
