@@ -56,6 +56,7 @@ struct SolverInfo {
   double bytes_per_pass_col, bytes_per_pass_row;
   int launches_per_step;
   std::int64_t group;
+  std::int64_t row_chunk;  // three-level: M1 rows per L2-resident row-side chunk (0: whole view)
 };
 
 class Solver {

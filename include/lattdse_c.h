@@ -118,6 +118,7 @@ typedef struct lattdse_solver_info {
   double bytes_per_step, bytes_per_pass_col, bytes_per_pass_row;
   int launches_per_step;
   int64_t M2a;       /* three-level inner split of M2 (0: two-level) */
+  int64_t row_chunk; /* three-level: M1 rows per L2-resident row-side chunk (0: whole view) */
 } lattdse_solver_info;
 
 /* Builds the anti-aliasing norm table, potential samples and device state. */

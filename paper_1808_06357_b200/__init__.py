@@ -262,7 +262,8 @@ class _Info(C.Structure):
     _fields_ = [("n_total", C.c_int64), ("batch", C.c_int64), ("M", C.c_int64), ("M1", C.c_int64),
                 ("M2", C.c_int64), ("group", C.c_int64), ("rank", C.c_int), ("method", C.c_int),
                 ("bytes_per_step", C.c_double), ("bytes_per_pass_col", C.c_double),
-                ("bytes_per_pass_row", C.c_double), ("launches_per_step", C.c_int), ("M2a", C.c_int64)]
+                ("bytes_per_pass_row", C.c_double), ("launches_per_step", C.c_int), ("M2a", C.c_int64),
+                ("row_chunk", C.c_int64)]
 
 
 METHODS = {"circulant": 0, "bluestein": 1}

@@ -8,6 +8,7 @@
 
 #include "fft_pass.cuh"
 #include "pass_instantiate.cuh"
+#include "cluster_col.inl"
 
 using namespace lattdse_dev;
 
@@ -116,7 +117,102 @@ template <int AXIS, int L> int time_prod(long long nrows, long long ncols, int t
   return run<AXIS, L, G::B, G::NT, PROG_DOUBLE, AXIS == AX_ROW ? -1 : 1, mb>(nrows, ncols, tw, tw, -1, true);
 }
 
+// cluster COL pass (cluster_col.inl) vs the plain COL pass on an n x ncols
+// grid, PROG_DOUBLE with a full complex diagonal; then both timed
+template <int LLOC, int C, int B, int NT, int MINB>
+int run_cluster(long long ncols, bool timing) {
+  constexpr int L = LLOC * C;
+  const long long M = (long long)L * ncols;
+  std::mt19937_64 rng(11);
+  std::uniform_real_distribution<double> u(-1, 1);
+  std::vector<double2> x(M), diag(M);
+  for (auto& v : x) v = make_double2(u(rng), u(rng));
+  for (auto& v : diag) v = make_double2(u(rng), u(rng));
+  std::vector<double2> tl(L);
+  for (int k = 0; k < L; ++k) tl[k] = root(k, L);
+  std::vector<double2> st(std::max(1, plan_twiddles<LLOC>(nullptr)));
+  plan_twiddles<LLOC>(st.data());
+  std::vector<double2> pt(std::max(1, plan_twiddles<L>(nullptr))), pt2(std::max(1, plan_twiddles<L>(nullptr, true)));
+  plan_twiddles<L>(pt.data());
+  plan_twiddles<L>(pt2.data(), true);
+  double2 *d0, *d1, *dd, *dtl, *dst, *dpt, *dpt2;
+  CK(cudaMalloc(&d0, M * 16)); CK(cudaMalloc(&d1, M * 16)); CK(cudaMalloc(&dd, M * 16));
+  CK(cudaMalloc(&dtl, L * 16)); CK(cudaMalloc(&dst, st.size() * 16)); CK(cudaMalloc(&dpt, pt.size() * 16)); CK(cudaMalloc(&dpt2, pt2.size() * 16));
+  CK(cudaMemcpy(d0, x.data(), M * 16, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d1, x.data(), M * 16, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dd, diag.data(), M * 16, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dtl, tl.data(), L * 16, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dst, st.data(), st.size() * 16, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dpt, pt.data(), pt.size() * 16, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dpt2, pt2.data(), pt2.size() * 16, cudaMemcpyHostToDevice));
+  PassArgs a{};
+  a.in = d0; a.out = d0; a.in_bstride = a.out_bstride = M;
+  a.nvalid_in = a.nvalid_mid = a.nvalid_out = M;
+  a.ncols = (int)ncols; a.nlines = (int)ncols;
+  a.diag_kind = DG_CPLX; a.diag = dd;
+  a.tw_lo = dtl; a.fft_tw = dst;
+  auto fc = cluster_col_kernel<LLOC, C, B, NT, -1, MINB>;
+  const int smc = ClusterGeom<LLOC, C, B>::bytes;
+  CK(cudaFuncSetAttribute(fc, cudaFuncAttributeMaxDynamicSharedMemorySize, smc));
+  const dim3 gc((unsigned)(C * (ncols / B)), 1);
+  PassArgs p = a;
+  p.in = p.out = d1; p.fft_tw = dpt; p.fft_tw2 = dpt2; p.tw_lo = nullptr;
+  using G = lattdse::dev::Geometry<AX_COL, L>;
+  auto fp = fft_pass_kernel<AX_COL, L, G::B, G::NT, PROG_DOUBLE, -1, 1>;
+  const int smp = SmemGeom<L, G::B>::bytes;
+  CK(cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, smp));
+  const dim3 gp((unsigned)((ncols + G::B - 1) / G::B), 1);
+  fc<<<gc, NT, smc>>>(a);
+  CK(cudaGetLastError());
+  fp<<<gp, G::NT, smp>>>(p);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  std::vector<double2> g0(M), g1(M);
+  CK(cudaMemcpy(g0.data(), d0, M * 16, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(g1.data(), d1, M * 16, cudaMemcpyDeviceToHost));
+  double e = 0, mx = 0;
+  for (long long i = 0; i < M; ++i) {
+    e = std::max(e, std::abs(g0[i].x - g1[i].x) + std::abs(g0[i].y - g1[i].y));
+    mx = std::max(mx, std::abs(g1[i].x) + std::abs(g1[i].y));
+  }
+  const bool ok = e / mx < 1e-13;
+  std::printf("cluster L=%d (Lloc %d x C %d, B=%d NT=%d minb=%d) %lld cols: max|cluster-plain|/max = %.3e %s\n", L, LLOC, C, B,
+              NT, MINB, ncols, e / mx, ok ? "ok" : "MISMATCH");
+  if (timing) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int reps = 20;
+    float ms = 0;
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) fc<<<gc, NT, smc>>>(a);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    std::printf("TIME cluster L=%d Lloc=%d C=%d B=%d minb=%d: %.2f us/launch\n", L, LLOC, C, B, MINB, 1e3 * ms / reps);
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) fp<<<gp, G::NT, smp>>>(p);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    std::printf("TIME plain   L=%d B=%d NT=%d: %.2f us/launch\n", L, G::B, G::NT, 1e3 * ms / reps);
+  }
+  cudaFree(d0); cudaFree(d1); cudaFree(dd); cudaFree(dtl); cudaFree(dst); cudaFree(dpt); cudaFree(dpt2);
+  return ok ? 0 : 1;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "cluster") {
+    int bad = 0;
+    bad |= run_cluster<512, 8, 8, 256, 2>(64, false);
+    bad |= run_cluster<1024, 4, 4, 256, 2>(64, false);
+    bad |= run_cluster<512, 8, 8, 256, 2>(4096, true);
+    bad |= run_cluster<512, 8, 8, 256, 3>(4096, true);
+    bad |= run_cluster<1024, 4, 4, 256, 2>(4096, true);
+    bad |= run_cluster<1024, 4, 4, 256, 3>(4096, true);
+    std::printf(bad ? "SOME FAILED\n" : "ALL OK\n");
+    return bad;
+  }
   int bad = 0;
   if (argc > 1 && std::string(argv[1]) == "time") {
     // config-1 production geometry (1296 x 1620)

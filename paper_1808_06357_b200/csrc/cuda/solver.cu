@@ -33,6 +33,7 @@
 #include "lattdse/solver.hpp"
 #include "aaset_dev.hpp"
 #include "pass_registry.hpp"
+#include "cluster_col.hpp"
 
 using namespace lattdse_dev;
 
@@ -412,20 +413,26 @@ double cost_row(int L) {
 // measured at config-4 size (tools/c4_geom_sweep.sh, profiles/README.md):
 // first-level COL pass, and the row side (inner COL forward + ROW + inner
 // COL inverse); the inner COL passes run twice per step as single
-// transforms (~0.6 of a fused double pass each)
+// transforms (~0.6 of a fused double pass each). Re-measured (r1e) after
+// the persisting-L2 carve-out was dropped for tables beyond it: COL lengths
+// below 512 run four columns per CTA (64-byte row segments), which the
+// HBM-streaming first-level pass rewards (486: 17.4 vs 810: 29.9 ps).
 double cost_col3(int L) {
   switch (L) {
-    case 1458: return 29.3; case 810: return 30.1; case 243: return 30.6; case 486: return 31.9;
-    case 1296: return 33.8; case 648: return 37.3; case 1620: return 38.8; case 720: return 38.9;
-    case 972: return 40.6; default: return 1.5 * cost_col(L);
+    case 486: return 17.4; case 324: return 19.9; case 432: return 20.7; case 243: return 22.9;
+    case 648: return 26.7; case 972: return 26.7; case 405: return 27.1; case 1296: return 27.9;
+    case 1458: return 28.1; case 1620: return 29.0; case 810: return 29.9; case 540: return 33.1;
+    case 720: return 33.7; default: return 1.5 * cost_col(L);
   }
 }
 double cost_row3(int La, int Lb) {
   const long long k = (long long)La * 10000 + Lb;
   switch (k) {
-    case 12962048: return 52.5; case 21602048: return 52.6; case 16202048: return 53.0;
-    case 16201024: return 55.0; case 12961024: return 55.8; case 12151215: return 56.3;
-    case 21604096: return 57.8; case 10802048: return 58.2; case 17281728: return 60.6;
+    case 6484096: return 40.6; case 6482048: return 40.6; case 21602048: return 42.0; case 17281728: return 42.1;
+    case 21604096: return 42.7; case 20482160: return 43.4; case 12962048: return 45.2; case 16202048: return 45.9;
+    case 12964096: return 45.9; case 16204096: return 46.7; case 19442048: return 47.4; case 14582048: return 49.7;
+    case 12154096: return 52.0; case 12151215: return 53.6; case 10802048: return 53.8; case 10804096: return 54.5;
+    case 40962160: return 60.8; case 8102048: return 63.0; case 8104096: return 63.3;
     default: return 1.5 * (1.2 * cost_col(La) + cost_row(Lb));
   }
 }
@@ -452,6 +459,7 @@ struct Solver::Impl {
   // pass of length Mb); three = false: the ROW pass covers M2 directly
   bool three = false;
   long long Ma = 0, Mb = 0;
+  long long row_chunk = 0;  // three-level: M1 rows per L2-resident row-side chunk (0: whole view)
   int tw_shift = 0;
   bool pfa = false;                 // Good-Thomas layout (rank-1), else four-step
   long long forced_M1 = 0, forced_M2 = 0, forced_M2a = 0;
@@ -466,6 +474,8 @@ struct Solver::Impl {
   DBuf<unsigned short> nidx_perm;  // Good-Thomas: norm index in position order (sentinel = zero phase)
   DBuf<double2> Khat, B1hat, B2hat, chirp, chirp_c, chirp_n;
   DBuf<double2> tw_col, tw_row, tw_col2, tw_row2, tw_mid, tw_mid2, tw_lo, tw_hi, scal;
+  DBuf<double2> cc_tab;  // rank-2 cluster COL pass tables (cluster_col.hpp), empty when unused
+  int cc_lloc = 0;        // its rows per CTA (0: plain COL pass; opt-in LATTDSE_CLUSTER_COL)
   DBuf<double> partial;
   DBuf<char> flush;
   bool bluestein_tables = false;
@@ -706,9 +716,34 @@ struct Solver::Impl {
   // per row of the view: FFT_M2 . (x table) . IFFT_M2 (table in the layout
   // r1_row_fwd produces)
   void r1_row_mid(double2* w, const double2* table, long long nb) {
+    if (three && row_chunk > 0) return r1_row_mid_chunked(w, table, nb);
     if (three) r1_mid_fwd(w, nb);
     r1_row_pass(PROG_DOUBLE, -1, w, table, nb);
     if (three) r1_mid_inv(w, nb);
+  }
+  // three-level, opt-in: the row side's three passes on row_chunk rows of
+  // the M1 x M2 view at a time, so the chunk (row_chunk * 16 M2 bytes) can
+  // stay L2-resident between the inner COL forward, the ROW pass and the
+  // inner COL inverse (the state crosses HBM once on this side instead of
+  // three times; measured slower at config 4, see the option above)
+  void r1_row_mid_chunked(double2* w, const double2* table, long long nb) {
+    for (long long m = 0; m < nb; ++m)
+      for (long long r0 = 0; r0 < M1; r0 += row_chunk) {
+        const long long k = std::min<long long>(row_chunk, M1 - r0);
+        double2* wc = w + m * M + r0 * M2;
+        PassArgs f = mid_args(wc);
+        f.post_tw = 1;
+        launch_pass(AX_COL, (int)Ma, PROG_LOADDIAG, -1, f, Mb, k);
+        PassArgs a = base_args(AX_ROW);
+        a.in = a.out = wc;
+        a.in_bstride = a.out_bstride = M;
+        a.nvalid_in = a.nvalid_mid = a.nvalid_out = k * M2;
+        set_diag(a, table + r0 * M2);
+        launch_pass(AX_ROW, (int)Mb, PROG_DOUBLE, -1, a, k * M2 / Mb, 1);
+        PassArgs b = mid_args(wc);
+        b.pre_tw = 1;
+        launch_pass(AX_COL, (int)Ma, PROG_STOREDIAG, +1, b, Mb, k);
+      }
   }
   void r1_row_fwd(double2* w) {
     if (three) r1_mid_fwd(w, 1);
@@ -746,6 +781,20 @@ struct Solver::Impl {
     a.diag_kind = dkind;
     a.diag_idx = nidx.p;
     a.lut = dkind == DG_SCALAR ? scal.p : kin_lut.p;
+    if (prog == PROG_DOUBLE && cc_lloc > 0 && (dkind == DG_LUT16 || dkind == DG_NONE)) {
+      // long columns (config 2): one cluster of CTAs per column block, the
+      // column split across the cluster's shared memories (cluster_col.inl)
+      a.nlines = (int)n2;
+      for (long long b0 = 0; b0 < nb; b0 += 65535) {
+        PassArgs c = a;
+        c.in = a.in + b0 * a.in_bstride;
+        c.out = a.out + b0 * a.out_bstride;
+        LD_CK(dev::launch_cluster_col((int)n1, cc_lloc, sign, c, cc_tab.p, n2, std::min<long long>(65535, nb - b0), stream));
+        ++launches;
+        if (sync_check) LD_CK(cudaStreamSynchronize(stream));
+      }
+      return;
+    }
     launch_pass(AX_COL, (int)n1, prog, sign, a, n2, nb);
   }
 
@@ -941,6 +990,8 @@ struct Solver::Impl {
     up(tw_hi, root_table(M, nhi, nlo));
     std::vector<double2> s = {make_double2(1.0 / (double)N, 0.0)};
     up(scal, s);
+    if (rank == 2) cc_lloc = dev::cluster_col_lloc((int)n1, n2);
+    if (cc_lloc > 0) up(cc_tab, dev::cluster_col_tables((int)n1, cc_lloc));
     LD_CK(cudaStreamSynchronize(stream));
   }
 
@@ -1142,7 +1193,7 @@ struct Solver::Impl {
         long long k = 0;
         // middle steps (ROW, COL) in graph chunks: identical launches, so the
         // GPU runs them back to back without host launch latency
-        if (!pt && use_graphs && !sync_check) {
+        if (!pt && use_graphs && !sync_check && row_chunk == 0) {
           const long long chunks = (nsteps - 1) / kGraphSteps;
           if (chunks > 0) {
             cudaGraphExec_t& ge = graphs[{g0, gb}];
@@ -1255,7 +1306,9 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
     cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, s.device);
     cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, s.device);
     const long long want = 16LL * ((s.persist_mode & 1) ? s.M : 0) + 16LL * ((s.persist_mode & 2) ? s.M : 0);
-    const long long grant = std::min<long long>(want, maxp);
+    // a table far larger than the carve-out (config 4) would only pin its
+    // first window's worth and shrink the L2 the chunked row side streams in
+    const long long grant = want > 2LL * maxp ? 0 : std::min<long long>(want, maxp);
     cudaCtxResetPersistingL2Cache();  // drop persisting lines left by earlier work on this device
     if (grant > 0 && maxw > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)grant) == cudaSuccess) {
       s.persist_bytes = grant;
@@ -1277,6 +1330,17 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
     long long g = (long long)std::floor(budget / (16.0 * (double)s.M));
     s.group = std::max<long long>(1, std::min<long long>(g, s.batch));
     s.group = std::min<long long>(s.group, 65535);
+  }
+
+  if (s.three && s.rank == 1) {
+    // opt-in (LATTDSE_ROW_CHUNK = M1 rows per chunk): the three-level row
+    // side on L2-sized row chunks. Measured slower on config 4 (row side 105
+    // vs 97 ms/step, profiles/README.md): the streaming passes are not
+    // HBM-bound, so the saved HBM round trips do not pay for 2430 short
+    // launches per step.
+    const char* e = std::getenv("LATTDSE_ROW_CHUNK");
+    const long long forced = e ? std::atoll(e) : 0;
+    if (forced > 0) s.row_chunk = std::min<long long>(forced, s.M1);
   }
 
   s.upload_twiddles();
@@ -1521,6 +1585,7 @@ SolverInfo Solver::info() const {
   i.M1 = s.M1;
   i.M2 = s.M2;
   i.M2a = s.three ? s.Ma : 0;
+  i.row_chunk = s.three ? s.row_chunk : 0;
   i.rank = s.rank;
   i.method = s.method + (s.rank == 1 ? (s.pfa ? "/good-thomas" : "/four-step") : "");
   i.group = s.group;
@@ -1536,10 +1601,13 @@ SolverInfo Solver::info() const {
     // position-ordered V_perm (M entries, mask folded in)
     i.bytes_per_pass_col = B * (32.0 * M + 16.0 * (s.pfa ? M : N));
     // state R+W + K^ once per group; three-level: the "row" side is three
-    // passes (inner COL forward, ROW with K^, inner COL inverse)
-    i.bytes_per_pass_row = (s.three ? 3.0 : 1.0) * B * 32.0 * M + groups * 16.0 * M;
+    // passes (inner COL forward, ROW with K^, inner COL inverse), which cross
+    // HBM once in total when they run on L2-resident row chunks
+    const bool chunked = s.three && s.row_chunk > 0;
+    i.bytes_per_pass_row = ((s.three && !chunked) ? 3.0 : 1.0) * B * 32.0 * M + groups * 16.0 * M;
     i.bytes_per_step = i.bytes_per_pass_col + i.bytes_per_pass_row;
-    i.launches_per_step = (s.three ? 4 : 2) * (int)groups;
+    const long long nchunks = chunked ? (s.M1 + s.row_chunk - 1) / s.row_chunk : 1;
+    i.launches_per_step = (int)((chunked ? 1 + 3 * nchunks * s.group : (s.three ? 4 : 2)) * (long long)groups);
   } else {
     const double G = (double)s.group, groups = std::ceil(B / G);
     i.bytes_per_pass_col = B * (32.0 * M + 9.0 * N);   // avg of (V 16N) and (D idx 2N)

@@ -510,6 +510,7 @@ int lattdse_solver_info_get(lattdse_solver* s, lattdse_solver_info* out) {
     out->bytes_per_pass_row = i.bytes_per_pass_row;
     out->launches_per_step = i.launches_per_step;
     out->M2a = i.M2a;
+    out->row_chunk = i.row_chunk;
   });
 }
 

@@ -187,6 +187,25 @@ def test_config2_first_step():
     assert abs(S.l2_norm()[0] - 1.0) <= TOL_NORM
 
 
+@pytest.mark.parametrize("cluster", ["8", "4"])
+def test_config2_cluster_col_opt_in(cluster, monkeypatch):
+    """Config 2 with the opt-in cluster COL pass (LATTDSE_CLUSTER_COL: each
+    4096-long column split over a cluster of 8 or 4 CTAs through distributed
+    shared memory, cluster_col.inl) against the oracle."""
+    monkeypatch.setenv("LATTDSE_CLUSTER_COL", cluster)
+    cfg = configs.CONFIGS["C2"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    S, orc = make(lat, a, b, c, p, cfg.sigma, cfg.eps, cfg.dt)
+    g, u0, u1 = oracle_coeffs(orc, c[0], p[0], cfg.sigma, 1)
+    S.step(1)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u1) <= TOL_ONE
+    u3 = orc.steps(u1, 2)
+    S.step(2)
+    assert rel(S.get_state(L.COEFFICIENTS)[0], u3) <= TOL_RUN
+    assert abs(S.l2_norm()[0] - 1.0) <= TOL_NORM
+
+
 def test_config3_members_vs_oracle():
     cfg = configs.CONFIGS["C3"]
     lat = configs.lattice(cfg)
@@ -251,16 +270,22 @@ def make_geom(lat, a, b, c, p, sigma, eps, dt, geometry, method="circulant"):
     return S, orc
 
 
+@pytest.mark.parametrize("chunk", [0, 1, 5])
 @pytest.mark.parametrize("method", ["circulant", "bluestein"])
 @pytest.mark.parametrize("geom", [(16, 24, 27), (9, 32, 32), (27, 9, 48)])
-def test_three_level_forced(geom, method):
+def test_three_level_forced(geom, method, chunk, monkeypatch):
     """Three-level rank-1 layout (M = M1 x Ma x Mb: COL pass, then a COL pass
-    inside every row and a ROW pass) forced at a small N against the oracle."""
+    inside every row and a ROW pass) forced at a small N against the oracle;
+    chunk > 0 forces the L2-chunked row side (chunk rows of the M1 x M2 view
+    at a time; 5 leaves a ragged last chunk), the opt-in LATTDSE_ROW_CHUNK."""
+    if chunk:
+        monkeypatch.setenv("LATTDSE_ROW_CHUNK", str(chunk))
     lat, a, b, c, p = configs.small_rank1(2, 4099, seed=31)
     eps, dt, sigma = 0.1, 1.0 / 64, 0.1
     S, orc = make_geom(lat, a, b, c, p, sigma, eps, dt, geom, method)
     info = S.info()
     assert (info["M1"], info["M2a"], info["M2"]) == (geom[0], geom[1], geom[1] * geom[2])
+    assert info["row_chunk"] == chunk
     g, u0, u1 = oracle_coeffs(orc, c[0], p[0], sigma, 1)
     assert rel(S.get_state(L.COEFFICIENTS)[0], u0) <= 1e-13
     S.step(1)
