@@ -282,6 +282,15 @@ int main(int argc, char** argv) {
       run<AX_ROW, 1728, 1, 224, PROG_DOUBLE, -1, 3>(1215, 1728, 0, 0, -1, true);
       run<AX_COL, 1215, 2, 272, PROG_DOUBLE, 1, 2>(1215, 1728, 1, 1, -1, true);
     }
+    if (argc > 2 && std::string(argv[2]) == "b8") {  // HBM-streaming short COL passes (config 4 first level): 4 vs 8 columns per CTA
+      time_prod<AX_COL, 486>(486, 1 << 20, 1);
+      run<AX_COL, 486, 8, 512, PROG_DOUBLE, 1, 1>(486, 1 << 20, 1, 1, -1, true);
+      run<AX_COL, 486, 8, 352, PROG_DOUBLE, 1, 1>(486, 1 << 20, 1, 1, -1, true);
+      time_prod<AX_COL, 324>(324, 1 << 20, 1);
+      run<AX_COL, 324, 8, 512, PROG_DOUBLE, 1, 1>(324, 1 << 20, 1, 1, -1, true);
+      time_prod<AX_COL, 432>(432, 1 << 20, 1);
+      run<AX_COL, 432, 8, 512, PROG_DOUBLE, 1, 1>(432, 1 << 20, 1, 1, -1, true);
+    }
     if (argc > 2 && std::string(argv[2]) == "c2") {  // config-2 column pass variants (4096 x 4096)
       run<AX_COL, 4096, 1, 256, PROG_DOUBLE, -1, 2>(4096, 4096, 0, 0, -1, true);
       run<AX_COL, 4096, 1, 256, PROG_DOUBLE, -1, 1>(4096, 4096, 0, 0, -1, true);
