@@ -36,14 +36,14 @@ int variant() {
 }
 int minb() {
   const char* e = std::getenv("LATTDSE_CLUSTER_MINB");
-  return e ? std::atoi(e) : 3;
+  return e ? std::atoi(e) : 2;
 }
 }  // namespace
 
 int cluster_col_lloc(int L, long long ncols) {
   const int c = variant();
-  if (L != 4096 || (c != 8 && c != 4)) return 0;
-  const int B = c;  // B = C columns per cluster (8: 128-byte, 4: 64-byte row segments)
+  if (L != 4096 || (c != 8 && c != 4 && c != 2)) return 0;
+  const int B = c;  // B = C columns per cluster (8: 128-byte, 4: 64-byte, 2: 32-byte row segments)
   if (ncols % B != 0) return 0;
   return L / c;
 }
@@ -60,6 +60,8 @@ std::vector<double2> cluster_col_tables(int L, int lloc) {
     for (int s = 0; s < Plan<512>::nst; ++s) radix[nst++] = Plan<512>::radix(s);
   } else if (lloc == 1024) {
     for (int s = 0; s < Plan<1024>::nst; ++s) radix[nst++] = Plan<1024>::radix(s);
+  } else if (lloc == 2048) {
+    for (int s = 0; s < Plan<2048>::nst; ++s) radix[nst++] = Plan<2048>::radix(s);
   }
   const int n = std::max(1, build_stage_twiddles(radix, nst, nullptr));
   std::vector<double2> st(n, make_double2(1.0, 0.0));
@@ -85,6 +87,13 @@ cudaError_t launch_cluster_col(int L, int lloc, int sign, const PassArgs& a, con
                 : launch_one<1024, 4, 4, 256, -1, 2>(a, tables, ncols, nbatch, s);
     return m3 ? launch_one<1024, 4, 4, 256, +1, 3>(a, tables, ncols, nbatch, s)
               : launch_one<1024, 4, 4, 256, +1, 2>(a, tables, ncols, nbatch, s);
+  }
+  if (lloc == 2048) {
+    if (sign < 0)
+      return m3 ? launch_one<2048, 2, 2, 256, -1, 3>(a, tables, ncols, nbatch, s)
+                : launch_one<2048, 2, 2, 256, -1, 2>(a, tables, ncols, nbatch, s);
+    return m3 ? launch_one<2048, 2, 2, 256, +1, 3>(a, tables, ncols, nbatch, s)
+              : launch_one<2048, 2, 2, 256, +1, 2>(a, tables, ncols, nbatch, s);
   }
   return cudaErrorInvalidValue;
 }

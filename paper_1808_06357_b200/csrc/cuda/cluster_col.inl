@@ -60,23 +60,33 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, MINB)
   constexpr int L = G::L;
   constexpr int TPT = (G::TASKS + NT - 1) / NT;
 
-  // ---- phase A: global -> radix-C DFT over the blocks -> twiddle -> DSMEM
+  // ---- phase A: global -> radix-C DFT over the blocks -> twiddle -> DSMEM.
+  // All of a thread's global loads are issued before any DSMEM store: the
+  // stores go through generic pointers the compiler cannot disambiguate
+  // from `in`, so interleaving them would serialise one HBM round trip per
+  // task (ncu: long-scoreboard stalls 12 per issued instruction).
   {
     const double2* in = a.in + bat * a.in_bstride;
+    double2 x[TPT][C];
 #pragma unroll
     for (int t = 0; t < TPT; ++t) {
       const int q = threadIdx.x + t * NT;
       if (G::TASKS % NT != 0 && q >= G::TASKS) break;
       const int b = q % B, i = r * G::SLICE + q / B;
-      double2 x[C];
 #pragma unroll
-      for (int k = 0; k < C; ++k) x[k] = in[(long long)(k * LLOC + i) * a.ncols + col0 + b];
-      DFT<C, SIGN>::run(x);
+      for (int k = 0; k < C; ++k) x[t][k] = in[(long long)(k * LLOC + i) * a.ncols + col0 + b];
+    }
+#pragma unroll
+    for (int t = 0; t < TPT; ++t) {
+      const int q = threadIdx.x + t * NT;
+      if (G::TASKS % NT != 0 && q >= G::TASKS) break;
+      const int b = q % B, i = r * G::SLICE + q / B;
+      DFT<C, SIGN>::run(x[t]);
       Pow<C> pw;
       pw.init(__ldg_d2(tw + i), C > 4 ? __ldg_d2(tw + ((4 * i) % L)) : make_double2(1.0, 0.0), make_double2(1.0, 0.0));
       sfor<C>([&](auto kc) {
         constexpr int ka = decltype(kc)::value;
-        double2 v = x[ka];
+        double2 v = x[t][ka];
         if constexpr (ka > 0) {
           const double2 w = pw.template get<ka>();
           v = SIGN < 0 ? c_mul(v, w) : c_mulc(v, w);
@@ -91,42 +101,64 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, MINB)
   // ---- phase B: local FFT_Lloc, x D at k1 = r + C kb, local IFFT_Lloc
   Cx c{lattdse_smem, a, col0, bat};
   run_fft<DevExec, AX_COL, LLOC, B, NT, PROG_DOUBLE, SIGN, SRC_SMEM, DST_SMEM>(c);
-  for (int q = threadIdx.x; q < B * LLOC; q += NT) {
-    const int b = q % B, kb = q / B;
-    const long long j = (long long)(r + C * kb) * a.ncols + col0 + b;
-    double2& v = lattdse_smem[Cx::slot(b, kb)];
-    if (a.diag_kind == DG_LUT16)
-      v = c_mul(v, __ldg_d2(a.lut + ((const unsigned short*)a.diag_idx)[j]));
-    else if (a.diag_kind == DG_CPLX)
-      v = c_mul(v, __ldg_d2(a.diag + j));
+  {
+    // diagonal coefficients fetched as one batch per thread, then applied
+    constexpr int PER = (B * LLOC + NT - 1) / NT;
+    double2 dg[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int q = threadIdx.x + u * NT;
+      dg[u] = make_double2(1.0, 0.0);
+      if ((B * LLOC) % NT != 0 && q >= B * LLOC) break;
+      const int b = q % B, kb = q / B;
+      const long long j = (long long)(r + C * kb) * a.ncols + col0 + b;
+      if (a.diag_kind == DG_LUT16)
+        dg[u] = __ldg_d2(a.lut + ((const unsigned short*)a.diag_idx)[j]);
+      else if (a.diag_kind == DG_CPLX)
+        dg[u] = __ldg_d2(a.diag + j);
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int q = threadIdx.x + u * NT;
+      if ((B * LLOC) % NT != 0 && q >= B * LLOC) break;
+      double2& v = lattdse_smem[Cx::slot(q % B, q / B)];
+      v = c_mul(v, dg[u]);
+    }
   }
   __syncthreads();
   run_fft<DevExec, AX_COL, LLOC, B, NT, PROG_DOUBLE, -SIGN, SRC_SMEM, DST_SMEM>(c);
   cl.sync();
 
   // ---- phase C: DSMEM -> untwiddle -> radix-C inverse DFT -> global
+  // (all DSMEM loads first, for the same reason as phase A)
   {
     double2* out = a.out + bat * a.out_bstride;
+    double2 z[TPT][C];
 #pragma unroll
     for (int t = 0; t < TPT; ++t) {
       const int q = threadIdx.x + t * NT;
       if (G::TASKS % NT != 0 && q >= G::TASKS) break;
       const int b = q % B, i = r * G::SLICE + q / B;
-      double2 z[C];
 #pragma unroll
-      for (int k = 0; k < C; ++k) z[k] = cl.map_shared_rank(lattdse_smem, k)[Cx::slot(b, i)];
+      for (int k = 0; k < C; ++k) z[t][k] = cl.map_shared_rank(lattdse_smem, k)[Cx::slot(b, i)];
+    }
+#pragma unroll
+    for (int t = 0; t < TPT; ++t) {
+      const int q = threadIdx.x + t * NT;
+      if (G::TASKS % NT != 0 && q >= G::TASKS) break;
+      const int b = q % B, i = r * G::SLICE + q / B;
       Pow<C> pw;
       pw.init(__ldg_d2(tw + i), C > 4 ? __ldg_d2(tw + ((4 * i) % L)) : make_double2(1.0, 0.0), make_double2(1.0, 0.0));
       sfor<C>([&](auto kc) {
         constexpr int ka = decltype(kc)::value;
         if constexpr (ka > 0) {
           const double2 w = pw.template get<ka>();
-          z[ka] = SIGN < 0 ? c_mulc(z[ka], w) : c_mul(z[ka], w);
+          z[t][ka] = SIGN < 0 ? c_mulc(z[t][ka], w) : c_mul(z[t][ka], w);
         }
       });
-      DFT<C, -SIGN>::run(z);
+      DFT<C, -SIGN>::run(z[t]);
 #pragma unroll
-      for (int k = 0; k < C; ++k) out[(long long)(k * LLOC + i) * a.ncols + col0 + b] = z[k];
+      for (int k = 0; k < C; ++k) out[(long long)(k * LLOC + i) * a.ncols + col0 + b] = z[t][k];
     }
   }
   cl.sync();  // keep this CTA's tile alive until every peer has read it

@@ -187,7 +187,7 @@ def test_config2_first_step():
     assert abs(S.l2_norm()[0] - 1.0) <= TOL_NORM
 
 
-@pytest.mark.parametrize("cluster", ["8", "4"])
+@pytest.mark.parametrize("cluster", ["8", "4", "2"])
 def test_config2_cluster_col_opt_in(cluster, monkeypatch):
     """Config 2 with the opt-in cluster COL pass (LATTDSE_CLUSTER_COL: each
     4096-long column split over a cluster of 8 or 4 CTAs through distributed
