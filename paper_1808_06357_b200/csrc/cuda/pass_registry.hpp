@@ -39,5 +39,6 @@ double cost_col(int L);
 double cost_row(int L);
 double cost_col3(int L);
 double cost_row3(int La, int Lb);
+double cost_pair_ensemble(int L1, int L2);
 
 }  // namespace lattdse::dev

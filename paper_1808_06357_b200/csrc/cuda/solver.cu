@@ -425,6 +425,16 @@ double cost_col3(int L) {
     case 720: return 33.7; default: return 1.5 * cost_col(L);
   }
 }
+// ensembles of >= 64 members stepped in one group (config 3, M = 524880):
+// measured ps per element per Strang step of the (COL L1, ROW L2) pair
+// (tools/c3_group_sweep.sh, profiles/README.md); -1 = not measured
+double cost_pair_ensemble(int L1, int L2) {
+  const long long k = (long long)L1 * 10000 + L2;
+  switch (k) {
+    case 10800486: return 28.0; case 4861080: return 28.5; case 7290720: return 34.2; case 9720540: return 34.8;
+    default: return -1.0;
+  }
+}
 double cost_row3(int La, int Lb) {
   const long long k = (long long)La * 10000 + Lb;
   switch (k) {
@@ -942,7 +952,9 @@ struct Solver::Impl {
       for (int L2 : dev::pass_lengths(AX_ROW)) {
         const long long m = (long long)L1 * L2;
         if (m < need || (double)m > 1.005 * (double)mmin) continue;
-        const double cost = (double)m * (col_cost(L1) + row_cost(L2));
+        // ensembles: measured pair costs where known (config 3's length)
+        const double pe = batch >= 64 ? dev::cost_pair_ensemble(L1, L2) : -1.0;
+        const double cost = (double)m * (pe > 0 ? pe : col_cost(L1) + row_cost(L2));
         if (best < 0 || cost < bcost) { best = m; b1 = L1; b2 = L2; bcost = cost; }
         if (std::gcd(L1, L2) == 1 && (bestp < 0 || cost < pcost)) { bestp = m; p1 = L1; p2 = L2; pcost = cost; }
       }
@@ -1321,13 +1333,17 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
 
   // L2-resident ensemble groups: work buffers of the group + shared tables
   // within ~70% of L2.
-  if (opt.group > 0) {
-    s.group = std::min<long long>(opt.group, s.batch);
+  const long long env_group = std::getenv("LATTDSE_GROUP") ? std::atoll(std::getenv("LATTDSE_GROUP")) : 0;  // experiments
+  if (opt.group > 0 || env_group > 0) {
+    s.group = std::min<long long>(opt.group > 0 ? opt.group : env_group, s.batch);
   } else {
-    int l2 = 0;
-    LD_CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s.device));
-    const double budget = 0.7 * l2 - 16.0 * (double)s.M - 16.0 * (double)s.N;
-    long long g = (long long)std::floor(budget / (16.0 * (double)s.M));
+    // every member in one group when the work buffers fit a quarter of the
+    // free HBM: wider launches beat L2-resident groups (config 3: 7533 us per
+    // step with all 512 members vs 8232 us with the L2-sized group of 9,
+    // profiles/README.md) because the passes are not HBM-bound
+    size_t free_b = 0, total_b = 0;
+    LD_CK(cudaMemGetInfo(&free_b, &total_b));
+    long long g = (long long)std::floor(0.25 * (double)free_b / (16.0 * (double)s.M));
     s.group = std::max<long long>(1, std::min<long long>(g, s.batch));
     s.group = std::min<long long>(s.group, 65535);
   }
