@@ -1,13 +1,12 @@
 """Fold ncu DRAM captures of configs 2-4 into profiles/ncu_traffic.json.
 
 Reads gpurun_out/<tag>/{C2,C3,C4}_traffic.csv (ncu_traffic.sh) and the
-matching *_plain.json bench lines. Step kernels are the fft_pass_kernel
-instances whose fifth template argument (program) is 0; the COL pass is the
-one whose first argument is 1 and length is the solver's M1, every other step
-kernel belongs to the row side. Per-launch traffic is dram read + write; the
-row side of a three-level geometry (config 4) is several launches, so its
-entry is the mean per row-side launch times (launches_per_step - 1), matching
-how bench.py's pass_ms["row"] covers the whole row side.
+matching *_plain.json bench lines. The step COL pass is the
+fft_pass_kernel instance whose first template argument is 1 (COL), length the
+solver's M1 and program (fifth argument) 0; the row side of that step is the
+launches_per_step - 1 launches right before it (one ROW pass, or at config 4's
+three-level geometry COL-Ma, ROW-Mb, COL-Ma), matching how bench.py's
+pass_ms["row"] covers the whole row side. Traffic is dram read + write.
 
     python paper_1808_06357_b200/tools/ncu_traffic.py r1g
 """
@@ -48,20 +47,21 @@ def main(tag):
             continue
         line = json.loads(open(jp).read().strip().splitlines()[-1])
         m1, lps = line["solver"]["M1"], line["solver"]["launches_per_step"]
-        col, row = [], []
+        launches = []
         for name, v in load(csvp):
             t = re.search(r"fft_pass_kernel<([^>]*)>", name)
-            if not t:
-                continue
-            args = [a.strip() for a in t.group(1).split(",")]
-            if args[4] != "0":
-                continue
-            b = v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum", 0.0)
-            (col if args[0] == "1" and int(args[1]) == m1 else row).append(b)
+            if t:
+                args = [a.strip() for a in t.group(1).split(",")]
+                b = v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum", 0.0)
+                launches.append((args[0] == "1" and int(args[1]) == m1 and args[4] == "0", b))
+        cols = [i for i, (is_col, _) in enumerate(launches) if is_col]
+        col = [launches[i][1] for i in cols]
+        # the row side of one step = the lps-1 launches right before a step COL launch
+        row = [sum(b for _, b in launches[i - (lps - 1):i]) for i in cols if i >= lps - 1]
         if col:
             table[f"{cfg}_circulant_col"] = sum(col) / len(col)
         if row:
-            table[f"{cfg}_circulant_row"] = sum(row) / len(row) * max(1, lps - 1)
+            table[f"{cfg}_circulant_row"] = sum(row) / len(row)
         print(cfg, "col", col, "row", row)
     json.dump(table, open(out_path, "w"), indent=1)
     print(json.dumps(table, indent=1))
