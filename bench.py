@@ -1,32 +1,42 @@
 """Benchmark of the Strang time-stepping hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C1] [--method circulant|bluestein]
+                    [--config C3] [--method circulant|bluestein]
 
-Workload (config.workload): BASELINE.json configs[1] = C1, d=6 rank-1
-lattice, N = 1048583 (smallest prime >= 2^20), eps=0.05, T=1, m=1024, one
-complex fp64 wave function. One bench step = one full propagation
-(m = 1024 Strang steps) of that wave function. L2 is flushed
-(512 MiB memset) before every timed bench step, outside its event pair.
+Workload (config.workload): BASELINE.json configs[3] = C3, the configuration
+the metric ("... 1/2/4/8 B200") is quoted on and the largest that runs on one
+GPU: 512 independent wave functions, d=6 rank-1 lattice, N = 262147 (smallest
+prime >= 2^18), eps=0.05, T=0.5, m=512, shared z and v. One bench step = one
+full propagation (m = 512 Strang steps) of every member.
+L2 is flushed (512 MiB memset) before every timed bench step, outside its
+event pair; a member group's working set (4.3 GB) is far beyond L2 anyway.
 
-value    : lattice-point Strang steps/s = N * m * ranks / (max over ranks of the
-           summed device time of the K steps), CUDA events on the solver stream.
+value    : lattice-point Strang steps/s = N * members * m * K / (max over ranks
+           of the summed device time of the K steps), CUDA events on the solver
+           stream. --gpus N shards the 512 members over N ranks (no data-path
+           collective); without WORLD_SIZE in the environment
+           bench.py launches the N ranks itself through torch.distributed.run.
 e2e      : the same metric through the public API with host buffers: per step
            set_state from pinned host memory (H2D), step(m), get_state (D2H),
-           wall clock around the synchronous calls.
-roofline : dominant pass kernel, algorithmic bytes per launch / its average
-           event-timed duration, against MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline: the CPU oracle (oracle/, a port of the reference spec -- the
-           reference itself has no solver) on this host's cores, bounded sample.
---impl reference: that CPU port on all host threads, same metric and config.
-N > 1 (torchrun): C1 does not shard -- every rank runs an independent replica
-("replicas only"); barrier + max over ranks.
+           wall clock around the synchronous calls, max over ranks.
+roofline : dominant pass kernel, algorithmic bytes per launch (every member's
+           state read and written once + the shared diagonal table once) / its
+           average event-timed duration, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline: rank 0 at N=1 only, bounded samples on this host's cores: the
+           oracle's literal Strang step with scipy.fft (pocketfft) transforms
+           on all threads (the value), plus single-thread, circulant-form and
+           C++-oracle datapoints (oracle/, a port of the reference's specified
+           solver -- the reference itself has no solver).
+--impl reference: that CPU port on all host threads, rank 0 only, inputs from
+           oracle/ alone (oracle/cases.py lattices and seeds, the oracle's own
+           shell-walk norm table) -- nothing from the product package.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -49,6 +59,17 @@ def measured_hbm_peak():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class Clocks:
@@ -101,7 +122,7 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def dist_setup(n_gpus):
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -109,8 +130,11 @@ def dist_setup(n_gpus):
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl")
+        else:
+            dist.init_process_group("gloo")
         return world, rank, local, dist, torch
     return 1, 0, 0, None, None
 
@@ -119,19 +143,11 @@ def _dev(dist):
     return "cuda" if dist.get_backend() == "nccl" else "cpu"
 
 
-def max_over_ranks(x, dist, torch):
+def reduce_over_ranks(x, dist, torch, op="max"):
     if dist is None:
         return x
     t = torch.tensor([x], dtype=torch.float64, device=_dev(dist))
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
-
-
-def sum_over_ranks(x, dist, torch):
-    if dist is None:
-        return x
-    t = torch.tensor([x], dtype=torch.float64, device=_dev(dist))
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
 
 
@@ -140,106 +156,201 @@ def barrier(dist):
         dist.barrier()
 
 
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def respawn(n):
+    """`bench.py --gpus N` without a launcher: run N ranks through
+    torch.distributed.run (one process per GPU), rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # ------------------------------------------------------------------ CPU port
-def cpu_port_rate(cfg, lat, norm2, a, b, c, p, steps_per_sample: int, samples: int = 1):
-    """CPU oracle (all threads): lattice-pt-steps/s over a bounded sample."""
-    from oracle.pyoracle import Oracle
-
-    gen, moduli = lat.generators()
-    orc = Oracle(gen, moduli, norm2, cfg.eps, a, b)
-    orc.set_dt(cfg.dt)
-    u = orc.analyze(orc.initial_samples(c[0], p[0], cfg.sigma))
-    orc.steps(u, 1)  # warm the plans
-    times = []
-    for _ in range(samples):
-        t0 = time.perf_counter()
-        u = orc.steps(u, steps_per_sample)
-        times.append(time.perf_counter() - t0)
-    return cfg.N * steps_per_sample / statistics.mean(times), times
+CPU_MAX_N = 1 << 25  # the CPU port runs configs up to this size; C4 uses C4r
 
 
-CPU_MAX_N = 1 << 25  # the CPU port is timed on configs up to this size
-
-
-def cpu_case(cfg):
-    """(config, lattice, norm table, a, b, c, p, note) the CPU port is timed on:
-    the workload itself, or -- config 4, whose single state is 17 GB and whose
-    CPU step takes minutes -- its reduced-N twin C4r (same d, eps, T, m,
-    sigma; N = 16777259), the rate being per lattice-point step either way."""
-    import paper_1808_06357_b200 as L
-    from paper_1808_06357_b200 import configs
+def cpu_case(name):
+    """(case, norm table, note) from oracle/ only: the config's lattice and
+    seeds restated in oracle/cases.py, the oracle's own shell-walk norm table.
+    Config 4 (17 GB per state) uses its reduced-N twin C4r."""
+    from oracle import pyoracle as po
+    from oracle.cases import CASES
 
     note = ""
-    if cfg.N > CPU_MAX_N and "C4r" in configs.CONFIGS:
-        cfg = configs.CONFIGS["C4r"]
+    if name == "C4":
+        name = "C4r"
         note = " (C4r: config 4's shape at N = 16777259; the full-N CPU step does not fit a bounded sample)"
-    lat = configs.lattice(cfg)
-    a, b, c, p = configs.problem(cfg, batch=1)
-    if cfg.rank == 1 and cfg.d > 8:
-        # d = 20: the host shell walk takes hours; the oracle's norm-table INPUT is
-        # built on the device (bit-identical to the host walk, tests/test_gpu_setup.py)
-        norm2, _ = L.aaset_norms_device(lat)
-    else:
-        norm2, _, _ = L.aaset_build(lat, with_vectors=False)
-    return cfg, lat, norm2, a, b, c, p, note
+    cs = CASES[name]
+    if not cs.gen[0]:
+        raise RuntimeError(f"{name}: no oracle-side generating vector")
+    norm2, _ = po.aaset(cs.gen, cs.moduli, with_vectors=False)
+    return cs, norm2, note
 
 
-def run_reference(args, cfg):
-    world, rank, _, dist, torch = dist_setup(args.gpus)
-    if rank != 0:
-        return 0
-    ccfg, lat, norm2, a, b, c, p, note = cpu_case(cfg)
-    sample = max(1, args.ref_sample_steps)
-    for _ in range(args.warmup):
-        cpu_port_rate(ccfg, lat, norm2, a, b, c, p, 1)
-    rate, times = cpu_port_rate(ccfg, lat, norm2, a, b, c, p, sample, samples=args.steps)
+class CpuPort:
+    """Bounded CPU samples of the workload (oracle/ only)."""
+
+    def __init__(self, name, workers=None):
+        from oracle import pyoracle as po
+        from oracle.scipy_port import ScipyPort
+
+        self.cs, norm2, self.note = cpu_case(name)
+        a, b, _ = self.cs.potential_params()
+        self.orc = po.Oracle(self.cs.gen, self.cs.moduli, norm2, self.cs.eps, a, b)
+        self.orc.set_dt(self.cs.dt)
+        self.port = ScipyPort(self.orc, self.cs.moduli, norm2, self.cs.eps, workers=workers)
+        self.port.set_dt(self.cs.dt)
+        c, p = self.cs.member(0)
+        self.g = self.orc.initial_samples(c, p, self.cs.sigma)
+        self.u = self.orc.analyze(self.g)
+
+    def rate(self, kind, steps):
+        """lattice-pt-steps/s of `steps` Strang steps of one wave function."""
+        t0 = time.perf_counter()
+        if kind == "literal":
+            self.port.steps(self.u, steps)
+        elif kind == "circulant":
+            self.port.circulant_steps(self.port.potH * self.g, steps)
+        elif kind == "oracle":
+            self.orc.steps(self.u, steps)
+        dt = time.perf_counter() - t0
+        return self.cs.N * steps / dt, dt
+
+    def sized(self, kind, seconds):
+        r1, t1 = self.rate(kind, 1)
+        steps = max(1, min(self.cs.m, int(seconds / max(t1, 1e-4))))
+        return steps
+
+
+def oracle_single_thread_rate(name, seconds):
+    """The C++ oracle on ONE thread, in a child process (OMP_NUM_THREADS=1)."""
+    code = ("import sys,json; sys.path.insert(0, %r); import bench; p = bench.CpuPort(%r, workers=1); "
+            "n = p.sized('oracle', %f); r, t = p.rate('oracle', n); print(json.dumps([r, n, t]))") % (ROOT, name, seconds)
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=900)
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline(name, seconds):
     cores = os.cpu_count()
+    p = CpuPort(name)
+    n = p.sized("literal", seconds)
+    rate, t = p.rate("literal", n)
+    p1 = CpuPort(name, workers=1)
+    n1 = p1.sized("literal", seconds / 2)
+    rate1, t1 = p1.rate("literal", n1)
+    extra = {"literal_1_thread": {"value": rate1, "steps": n1, "seconds": t1}}
+    if len(p.cs.moduli) == 1:
+        nc = p.sized("circulant", seconds / 2)
+        rc, tc = p.rate("circulant", nc)
+        extra["circulant_all_threads"] = {"value": rc, "steps": nc, "seconds": tc,
+                                          "note": "same operator as one length-M cyclic convolution per step"}
+    no = p.sized("oracle", seconds / 2)
+    ro, to = p.rate("oracle", no)
+    extra["cxx_oracle_all_threads"] = {"value": ro, "steps": no, "seconds": to,
+                                       "note": "oracle.cpp's own recursive FFT + Bluestein, OpenMP"}
+    try:
+        r, nn, tt = oracle_single_thread_rate(name, seconds / 2)
+        extra["cxx_oracle_1_thread"] = {"value": r, "steps": nn, "seconds": tt}
+    except Exception as e:  # noqa: BLE001
+        extra["cxx_oracle_1_thread"] = {"error": str(e)[:200]}
+    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+            "sample": f"{n} literal Strang steps (SPEC.md:336-344) of one {p.cs.name} wave function, oracle setup + "
+                      f"scipy.fft transforms on {cores} threads, {t:.1f} s{p.note}",
+            "datapoints": extra}
+
+
+def run_reference(args):
+    world, rank, _, dist, torch = dist_setup()
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return 0
+    cores = os.cpu_count()
+    p = CpuPort(args.config)
+    sample = p.sized("literal", args.ref_seconds)
+    for _ in range(args.warmup):
+        p.rate("literal", 1)
+    rates, times = [], []
+    for _ in range(args.steps):
+        r, t = p.rate("literal", sample)
+        rates.append(r)
+        times.append(t)
+    value = p.cs.N * sample * len(times) / sum(times)
     line = {
-        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128 (complex fp64)", "data": "synthetic (seeded BASELINE families)",
-        "config": config_dict(cfg, args, note=f"1 reference step = {sample} Strang steps of the workload (bounded sample)"),
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{sample} literal Strang steps of {ccfg.name} per bench step (4 length-N DFTs each), "
-                                   f"OpenMP on {cores} host threads{note}"},
-        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128 (complex fp64)",
+        "data": "synthetic (seeded BASELINE families, oracle/cases.py)",
+        "config": config_dict(args, note=f"1 reference step = {sample} Strang steps of one wave function "
+                                          "(bounded sample); rate per lattice-point step"),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+                         "sample": f"{sample} literal Strang steps of one {p.cs.name} wave function per bench step "
+                                   f"(4 length-N DFTs each, scipy.fft on {cores} threads){p.note}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
     return 0
 
 
-def config_dict(cfg, args, note=None):
-    d = {"workload": f"{cfg.name}: d={cfg.d} rank-{cfg.rank} N={cfg.N} eps={cfg.eps} T={cfg.T} m={cfg.m} "
-                     f"batch={cfg.batch}; 1 bench step = full propagation (m Strang steps)",
-         "lattice": "CBC prime-n generating vector (paper_1808_06357_b200/catalog.json)" if cfg.rank == 1
-         else "product rank-2 lattice (configs.py)",
-         "method": args.method, "l2": "flushed (512 MiB memset) before every timed bench step",
-         "parallelism": ("1 GPU" if args.gpus == 1 else
-                         ("ensemble sharded by member (shard_members), no data-path collective" if cfg.batch > 1
-                          else "replicas only (a single wave function of this size does not shard)"))}
+def config_dict(args, note=None, world=1):
+    from oracle.cases import CASES  # plain data; the same table as configs.py (tests/test_oracle_cases.py)
+
+    cs = CASES.get(args.config)
+    if cs is None:
+        wl = args.config
+    else:
+        wl = (f"{cs.name}: d={cs.d} rank-{len(cs.moduli)} N={cs.N} eps={cs.eps} T={cs.T} m={cs.m} "
+              f"members={cs.batch}; 1 bench step = full propagation (m Strang steps) of every member")
+    d = {"workload": wl, "method": args.method,
+         "l2": "flushed (512 MiB memset) before every timed bench step; per-pass working set >> L2",
+         "parallelism": ("1 GPU" if world == 1 else f"{world} GPUs: ensemble members sharded by rank "
+                         "(configs.shard_members), no data-path collective")}
     if note:
         d["note"] = note
     return d
 
 
 # ------------------------------------------------------------------ our arm
-def run_ours(args, cfg):
-    world, rank, local, dist, torch = dist_setup(args.gpus)
+def traffic_for(cfg_name, method, side, info):
+    """ncu DRAM bytes per launch from profiles/ncu_traffic.json, only when the
+    entry was captured on this geometry and kernel family (else null)."""
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        e = json.load(open(tp)).get(f"{cfg_name}_{method}_{side}")
+    except Exception:
+        return None, None
+    if not isinstance(e, dict):
+        return None, None
+    want = {"M1": info["M1"], "M2": info["M2"], "group": info["group"], "kernel": info.get("pass_kernel")}
+    if any(e.get(k) != v for k, v in want.items()):
+        return None, None
+    return e["bytes"], e.get("source")
+
+
+def run_ours(args):
+    world, rank, local, dist, torch = dist_setup()
     import paper_1808_06357_b200 as L
     from paper_1808_06357_b200 import configs
 
+    cfg = configs.CONFIGS[args.config]
     lat = configs.lattice(cfg)
     batch_total = cfg.batch if args.batch is None else args.batch
     a, b, c, p = configs.problem(cfg, batch=batch_total)
     if batch_total > 1:
-        # ensemble: shard members across ranks, no data-path collective
         m0, batch = configs.shard_members(batch_total, rank, world)
         c, p = c[m0:m0 + batch], p[m0:m0 + batch]
         members_all = batch_total
     else:
-        batch = 1  # single wave function: every rank runs a replica
+        batch = 1  # a single wave function: every rank runs a replica
         members_all = world
-    # rank-1: the solver builds its norm table on the device (setup, untimed)
     norm2 = None if cfg.rank == 1 else L.aaset_build(lat, with_vectors=False)[0]
     S = L.Solver(lat, cfg.eps, a, b, c, p, cfg.sigma, method=args.method, device=local, norm2=norm2)
     S.set_dt(cfg.dt)
@@ -264,77 +375,70 @@ def run_ours(args, cfg):
     launches = S.kernel_launches() - launches0
     clk = clocks.stop()
     barrier(dist)
-    total_ms = max_over_ranks(sum(per_step), dist, torch)
+    total_ms = reduce_over_ranks(sum(per_step), dist, torch)
     work = float(cfg.N) * members_all * m * args.steps
     value = work / (total_ms * 1e-3)
 
-    # ---- per-pass durations (instrumented run, outside the timed region)
+    # ---- per-pass durations (event-timed launches on the solver stream)
     S.flush_l2()
-    ms_col, ms_row = S.profile_passes(min(m, 256))
+    ms_col, ms_row = S.profile_passes(min(m, 64))
     peak, peak_kind = measured_hbm_peak()
-    dom = "col" if ms_col >= ms_row else "row"
-    dom_ms = ms_col if dom == "col" else ms_row
-    # info's per-pass bytes cover the whole batch; one launch covers one group
     groups = -(-batch // max(1, info["group"]))
-    dom_bytes = (info["bytes_per_pass_col"] if dom == "col" else info["bytes_per_pass_row"]) / groups
-    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get(f"{cfg.name}_{args.method}_{dom}")
-        except Exception:
-            traffic = None
+    pass_bytes = {"col": info["bytes_per_pass_col"] / groups, "row": info["bytes_per_pass_row"] / groups}
+    pass_ms = {"col": ms_col, "row": ms_row}
+    dom = "col" if ms_col >= ms_row else "row"
+    achieved = pass_bytes[dom] / (pass_ms[dom] * 1e-3) / 1e9
+    traffic, tsrc = traffic_for(cfg.name, args.method, dom, info)
     step_ms = statistics.mean(per_step) / m
-    canonical = (160.0 * info["M"] + 18.0 * info["n_total"]) * batch if cfg.rank == 1 else 82.0 * info["n_total"] * batch
+    step_bytes = info["bytes_per_step"]  # all members of this rank, every pass of one Strang step
+    canonical = ((160.0 * info["M"] + 18.0 * info["n_total"]) * batch if cfg.rank == 1
+                 else 82.0 * info["n_total"] * batch)
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": traffic, "kernel": f"{dom} pass (fft_pass_kernel, {'COL' if dom == 'col' else 'ROW'} axis)",
-        "bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms, "peak_kind": peak_kind,
-        "pass_ms": {"col": ms_col, "row": ms_row},
-        "note": (f"working set ~{info['bytes_per_step'] / 2 / 1e6:.0f} MB per pass: L2-resident across steps (126 MB L2); "
-                 "frac > 1 would mean L2 reuse, see DESIGN.md" if info["bytes_per_step"] / 2 < 100e6 else
-                 f"working set {info['bytes_per_step'] / 2 / 1e9:.1f} GB per pass streams through HBM"),
-        "step_vs_canonical": {
-            "canonical_bytes_per_step": canonical,
-            "canonical_model": "160*M*+18*N (4 Bluestein passes, SURVEY.md 8(d))" if cfg.rank == 1 else "82*N",
-            "t_roof_us_at_8TBps": canonical / 8e12 * 1e6, "measured_us_per_step": step_ms * 1e3,
-            "frac_of_canonical_roofline": (canonical / 8e12) / (step_ms * 1e-3)},
+        "traffic": traffic, "traffic_source": tsrc,
+        "kernel": f"{dom} pass ({info.get('pass_kernel', 'fft_pass')}, {'COL' if dom == 'col' else 'ROW'} axis)",
+        "bytes_per_launch": pass_bytes[dom], "avg_launch_ms": pass_ms[dom], "peak_kind": peak_kind,
+        "bytes_model": "every member's state read+written once per pass (32 B x M per member) + the shared "
+                       "diagonal table once per launch (V: 16 N, K^: 16 M)",
+        "passes": {s: {"ms": pass_ms[s], "bytes": pass_bytes[s],
+                       "frac": pass_bytes[s] / (pass_ms[s] * 1e-3) / 1e9 / peak} for s in ("col", "row")},
+        "step": {"bytes": step_bytes, "us": step_ms * 1e3,
+                 "frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak},
+        "extra_canonical_model": {
+            "note": "NOT a roofline fraction: SURVEY.md 8(d)'s literal 4-pass Bluestein bytes (160 M + 18 N per "
+                    "member) over the measured time of our 2-pass circulant step (an algorithm credit)",
+            "canonical_bytes_per_step": canonical, "t_roof_us_at_8TBps": canonical / 8e12 * 1e6},
     }
 
     # ---- e2e through the public API with pinned host buffers
-    e2e = None
-    if rank == 0 or world > 1:
-        import torch as _t
+    import torch as _t
 
-        n = cfg.N * batch
-        host_in = _t.empty(2 * n, dtype=_t.float64, pin_memory=True)
-        host_out = _t.empty(2 * n, dtype=_t.float64, pin_memory=True)
-        g = S.get_state()
-        host_in.numpy()[:] = g.reshape(-1).view(np.float64)
-        e2e_times = []
-        for _ in range(args.steps):
-            S.flush_l2()
-            t0 = time.perf_counter()
-            S.set_state_ptr(host_in.data_ptr(), batch)
-            S.step(m)
-            S.get_state_ptr(host_out.data_ptr(), batch)
-            e2e_times.append(time.perf_counter() - t0)
-        e2e_s = max_over_ranks(sum(e2e_times), dist, torch)
-        e2e = {"value": float(cfg.N) * members_all * m * args.steps / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
-               "ms_per_step": 1e3 * e2e_s / args.steps}
+    n = cfg.N * batch
+    host_in = _t.empty(2 * n, dtype=_t.float64, pin_memory=_t.cuda.is_available())
+    host_out = _t.empty(2 * n, dtype=_t.float64, pin_memory=_t.cuda.is_available())
+    g = S.get_state()
+    host_in.numpy()[:] = g.reshape(-1).view(np.float64)
+    e2e_times = []
+    barrier(dist)
+    for _ in range(args.steps):
+        S.flush_l2()
+        t0 = time.perf_counter()
+        S.set_state_ptr(host_in.data_ptr(), batch)
+        S.step(m)
+        S.get_state_ptr(host_out.data_ptr(), batch)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = reduce_over_ranks(sum(e2e_times), dist, torch)
+    e2e = {"value": float(cfg.N) * members_all * m * args.steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": 16 * cfg.N * members_all, "d2h_bytes_per_step": 16 * cfg.N * members_all,
+           "ms_per_step": 1e3 * e2e_s / args.steps}
 
-    # ---- CPU baseline (rank 0, N=1 only): oracle port, bounded sample
+    # ---- CPU baseline (rank 0, N=1 only): oracle ports, bounded samples
     cpu = None
     if world == 1 and not args.no_cpu:
-        ccfg, clat, cnorm2, ca, cb, cc, cp, note = cpu_case(cfg)
-        rate1, _ = cpu_port_rate(ccfg, clat, cnorm2, ca, cb, cc, cp, 1)
-        steps = max(1, min(64, int(args.cpu_seconds / max(ccfg.N / rate1, 1e-3))))
-        rate, times = cpu_port_rate(ccfg, clat, cnorm2, ca, cb, cc, cp, steps)
-        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-               "sample": f"{steps} literal Strang steps of {ccfg.name} (CPU oracle, OpenMP on {os.cpu_count()} threads), "
-                         f"{sum(times):.1f} s{note}"}
+        try:
+            cpu = cpu_baseline(cfg.name, args.cpu_seconds)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"error": str(e)[:300]}
 
     if rank == 0:
         line = {
@@ -342,9 +446,10 @@ def run_ours(args, cfg):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if batch_total > 1 else "weak", "vs_baseline": None, "dtype": "c128 (complex fp64)",
             "data": "synthetic (seeded BASELINE families, DESIGN.md Seeds)",
-            "config": config_dict(cfg, args), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches), "clocks": clk,
-            "solver": {k: info[k] for k in ("M", "M1", "M2", "group", "launches_per_step", "bytes_per_step")},
+            "config": config_dict(args, world=world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(reduce_over_ranks(launches, dist, torch, "sum")), "clocks": clk,
+            "solver": {k: info[k] for k in ("M", "M1", "M2", "group", "launches_per_step", "bytes_per_step")
+                       if k in info} | {"members_per_rank": batch, "pass_kernel": info.get("pass_kernel")},
             "us_per_strang_step": step_ms * 1e3,
         }
         print(json.dumps(line), flush=True)
@@ -354,25 +459,24 @@ def run_ours(args, cfg):
 
 
 # ------------------------------------------------------------- sharded arm
-def run_sharded(args, cfg):
+def run_sharded(args):
     """One wave function sharded over the ranks (DistSolver): NCCL exchanges
     between GPUs under torchrun, or --virtual-ranks G on one GPU."""
-    world, rank, local, dist, torch = dist_setup(args.gpus)
+    world, rank, local, dist, torch = dist_setup()
     import paper_1808_06357_b200 as L
     from paper_1808_06357_b200 import configs
 
+    cfg = configs.CONFIGS[args.config]
     lat = configs.lattice(cfg)
     a, b, c, p = configs.problem(cfg, batch=1)
-    norm2 = None  # rank-1: the norm table is built on the device (bit-identical to the host walk)
     if world > 1:
         uid = [L.DistSolver.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        D = L.DistSolver(lat, cfg.eps, a, b, c, p, cfg.sigma, world=world, rank=rank, device=local,
-                         nccl_id=uid[0], norm2=norm2)
+        D = L.DistSolver(lat, cfg.eps, a, b, c, p, cfg.sigma, world=world, rank=rank, device=local, nccl_id=uid[0])
         G = world
     else:
         G = max(1, args.virtual_ranks)
-        D = L.DistSolver(lat, cfg.eps, a, b, c, p, cfg.sigma, world=G, rank=-1, device=0, norm2=norm2)
+        D = L.DistSolver(lat, cfg.eps, a, b, c, p, cfg.sigma, world=G, rank=-1, device=0)
     D.set_dt(cfg.dt)
     D.discretize_initial()
     m = cfg.m if args.m is None else args.m
@@ -381,7 +485,7 @@ def run_sharded(args, cfg):
     barrier(dist)
     per = [D.time_steps(m) for _ in range(args.steps)]
     barrier(dist)
-    total_ms = max_over_ranks(sum(per), dist, torch)
+    total_ms = reduce_over_ranks(sum(per), dist, torch)
     norm = D.l2_norm()
     info = D.info()
     # per-rank algorithmic bytes per Strang step: COL pass R+W
@@ -392,7 +496,7 @@ def run_sharded(args, cfg):
     row_passes = 3 if info.get("Ma", 0) else 1
     hbm = 32.0 * slab + 16.0 * slab + row_passes * 32.0 * slab + 16.0 * slab
     nvl = 2.0 * 16.0 * info["M"] * (G - 1) / (G * G)
-    t_roof = hbm / (measured_hbm_peak()[0] * 1e9) + (nvl / 900e9 if world > 1 else 0.0)
+    t_roof = hbm / (measured_hbm_peak()[0] * 1e9) + (nvl / 770e9 if world > 1 else 0.0)
     t_meas = 1e-3 * total_ms / (args.steps * m)
     if rank == 0:
         line = {
@@ -400,14 +504,14 @@ def run_sharded(args, cfg):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (complex fp64)",
             "data": "synthetic (seeded BASELINE families, DESIGN.md Seeds)",
-            "config": {**config_dict(cfg, args), "parallelism": f"one wave function sharded over {G} ranks "
+            "config": {**config_dict(args, world=world), "parallelism": f"one wave function sharded over {G} ranks "
                        f"({'NCCL send/recv' if world > 1 else 'virtual ranks on one GPU, device copies'}), "
                        "2 block exchanges per Strang step"},
             "sharded": {**info, "ranks": G, "norm_after": norm},
             "roofline": {"bound": "hbm+nvlink", "hbm_bytes_per_rank_step": hbm, "nvlink_bytes_per_rank_step": nvl,
                          "t_roof_us": 1e6 * t_roof, "frac": t_roof / t_meas,
                          "note": "virtual ranks share one GPU's HBM: the exchange is device copies, not NVLink"
-                         if world == 1 else "HBM at MEASURED_PEAKS hbm_gbs, NVLink 900 GB/s per direction"},
+                         if world == 1 else "HBM at MEASURED_PEAKS hbm_gbs, NVLink at the measured 770 GB/s"},
             "us_per_strang_step": 1e3 * total_ms / (args.steps * m),
         }
         print(json.dumps(line), flush=True)
@@ -422,26 +526,25 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C1")
+    ap.add_argument("--config", default="C3")
     ap.add_argument("--method", default="circulant", choices=["circulant", "bluestein"])
     ap.add_argument("--batch", type=int, default=None, help="ensemble members (C3); default: the config's")
     ap.add_argument("--m", type=int, default=None, help="Strang steps per bench step (default: the config's m)")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-sample-steps", type=int, default=4)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0, help="CPU baseline: seconds per datapoint")
+    ap.add_argument("--ref-seconds", type=float, default=3.0, help="reference arm: seconds per bench step")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--shard", action="store_true", help="shard one wave function across the ranks (NCCL)")
     ap.add_argument("--virtual-ranks", type=int, default=0, help="sharded path with G virtual ranks on one GPU")
     args = ap.parse_args()
-    from paper_1808_06357_b200 import configs
-
-    cfg = configs.CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return respawn(args.gpus)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the timing rules ask for >= 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
-        return run_reference(args, cfg)
+        return run_reference(args)
     if args.shard or args.virtual_ranks > 0:
-        return run_sharded(args, cfg)
-    return run_ours(args, cfg)
+        return run_sharded(args)
+    return run_ours(args)
 
 
 if __name__ == "__main__":

@@ -11,7 +11,7 @@
 #include <vector>
 #include <string>
 
-#include "fft_pass.cuh"
+#include "fft_pass3.cuh"
 
 using namespace lattdse_dev;
 using cld = std::complex<long double>;
@@ -103,30 +103,30 @@ void emulate(PassArgs a, int nlines, int nbatch) {
     }
 }
 
-// v2 path: host copy of load_tile (zero-fill semantics) + SRC_TILE stages.
+// pass3 path: the dense TMA tile (COL [row][B], ROW [B][L]; columns
+// beyond the view zero-filled like the TMA bounds check) + SRC_TMA stages
+// over the tile buffer and the extra ping-pong buffer (fft_pass3.cuh).
 template <int AXIS, int L, int B, int NT, int SIGN1>
-void emulate_v2(PassArgs a, int nlines, int nbatch) {
-  using C = Ctx<AXIS, L, B, PROG_DOUBLE>;
-  std::vector<double2> sm(SmemGeom<L, B>::bytes / 16), dg(B * L);
+void emulate_v3(PassArgs a, int nlines, int nbatch) {
+  using G = Pass3Geom<AXIS, L, B>;
+  std::vector<double2> tile(G::buf_bytes / 16), wbuf(G::buf_bytes / 16);
   const int nblk = (nlines + B - 1) / B;
   for (int t = 0; t < nblk * nbatch; ++t) {
     const int line0 = (t % nblk) * B;
     const long long bat = t / nblk;
-    for (int q = 0; q < B * L; ++q) {
-      int b, i;
-      TileWalk<AXIS, L, B>::elem(q, b, i);
-      const bool live = line0 + b < a.nlines;
-      const long long j = AXIS == AX_ROW ? (long long)(line0 + b) * L + i : (long long)i * a.ncols + (line0 + b);
-      sm[C::slot(b, i)] = (live && j < a.nvalid_in) ? a.in[bat * a.in_bstride + j] : make_double2(0, 0);
-      dg[b * L + i] = (live && j < a.nvalid_mid) ? a.diag[j] : make_double2(0, 0);
-    }
-    C c{sm.data(), a, line0, bat, dg.data()};
-    run_pass<HostExec, AXIS, L, B, NT, PROG_DOUBLE, SIGN1, SRC_TILE>(c);
+    for (int b = 0; b < B; ++b)
+      for (int i = 0; i < L; ++i) {
+        const bool live = line0 + b < a.nlines;
+        const long long j = AXIS == AX_ROW ? (long long)(line0 + b) * L + i : (long long)i * a.ncols + (line0 + b);
+        tile[AXIS == AX_COL ? i * B + b : b * L + i] = live ? a.in[bat * a.in_bstride + j] : make_double2(0, 0);
+      }
+    Ctx<AXIS, L, B, PROG_DOUBLE> c{tile.data(), a, line0, bat, tile.data(), G::nbuf == 3 ? wbuf.data() : nullptr};
+    run_pass<HostExec, AXIS, L, B, NT, PROG_DOUBLE, SIGN1, SRC_TMA>(c);
   }
 }
 
-// v2 double program with a complex diag vs naive DFTs
-template <int AXIS, int L, int B, int NT, int SIGN1> void test_double_v2(int other, long long nmid, int pre, int post) {
+// pass3 double program with a complex diag vs naive DFTs
+template <int AXIS, int L, int B, int NT, int SIGN1> void test_double_v3(int other, long long nmid, int pre, int post) {
   int nrows = AXIS == AX_ROW ? other : L, ncols = AXIS == AX_ROW ? L : other;
   std::mt19937_64 rng(L * 29 + AXIS + 3);
   std::uniform_real_distribution<double> u(-1, 1);
@@ -155,7 +155,7 @@ template <int AXIS, int L, int B, int NT, int SIGN1> void test_double_v2(int oth
   a.tw_lo = tb.tw_lo.data();
   a.tw_hi = tb.tw_hi.data();
   a.tw_shift = tb.shift;
-  emulate_v2<AXIS, L, B, NT, SIGN1>(a, AXIS == AX_ROW ? nrows : ncols, 1);
+  emulate_v3<AXIS, L, B, NT, SIGN1>(a, AXIS == AX_ROW ? nrows : ncols, 1);
   auto tw = [&](long long t) {
     long double ang = -2.0L * kPi * (long double)(t % n) / (long double)n;
     return cld(cosl(ang), sinl(ang));
@@ -182,7 +182,7 @@ template <int AXIS, int L, int B, int NT, int SIGN1> void test_double_v2(int oth
     }
   }
   char buf[96];
-  std::snprintf(buf, sizeof buf, "v2 double axis=%d L=%d B=%d NT=%d sign=%+d", AXIS, L, B, NT, SIGN1);
+  std::snprintf(buf, sizeof buf, "pass3 double axis=%d L=%d B=%d NT=%d sign=%+d", AXIS, L, B, NT, SIGN1);
   check(buf, e / mx, 4e-16 * 60);
 }
 
@@ -457,13 +457,16 @@ int main(int argc, char** argv) {
     std::printf("c1 col entry emulated ok %f\n", buf[12345].x);
     return 0;
   }
-  if (argc > 1 && std::string(argv[1]) == "v2") {
-    test_double_v2<AX_ROW, 1728, 1, 192, -1>(2, 3000, 0, 0);
-    test_double_v2<AX_COL, 1215, 2, 288, 1>(5, 2000, 1, 1);
-    test_double_v2<AX_ROW, 64, 4, 64, 1>(6, 300, 0, 0);
-    test_double_v2<AX_COL, 256, 4, 128, -1>(6, 900, 1, 1);
-    test_double_v2<AX_ROW, 4096, 1, 256, 1>(1, 3000, 0, 0);
-    test_double_v2<AX_COL, 720, 2, 160, 1>(3, 1500, 1, 0);
+  if (argc > 1 && std::string(argv[1]) == "v3") {
+    test_double_v3<AX_ROW, 1728, 1, 192, -1>(2, 3000, 0, 0);
+    test_double_v3<AX_COL, 1215, 2, 288, 1>(5, 2000, 1, 1);
+    test_double_v3<AX_ROW, 64, 4, 64, 1>(6, 300, 0, 0);
+    test_double_v3<AX_COL, 256, 4, 128, -1>(6, 900, 1, 1);
+    test_double_v3<AX_ROW, 4096, 1, 256, 1>(1, 3000, 0, 0);
+    test_double_v3<AX_COL, 720, 2, 160, 1>(3, 1500, 1, 0);
+    test_double_v3<AX_COL, 1080, 2, 384, 1>(7, 5000, 1, 1);
+    test_double_v3<AX_ROW, 486, 1, 96, -1>(3, 1000, 0, 0);
+    test_double_v3<AX_COL, 486, 4, 192, -1>(6, 2000, 1, 1);
     std::printf(g_fail ? "SOME FAILED\n" : "ALL OK\n");
     return g_fail;
   }

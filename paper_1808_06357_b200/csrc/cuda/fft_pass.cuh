@@ -16,11 +16,11 @@
 // Two kernel shapes share the stage code:
 //  fft_pass_kernel  (v1): one CTA per tile of B lines; stage 0 loads straight
 //                   from global, the last stage stores straight to global.
-//  fft_pass2_kernel (v2, the hot PROG_DOUBLE + complex-diag passes):
-//                   persistent CTAs; tile t+1's lines and its diagonal-table
-//                   tile are prefetched with cp.async into a second shared
-//                   buffer while tile t is transformed, so the L2/HBM latency
-//                   is off the critical path.
+//  fft_pass3_kernel (fft_pass3.cuh, the per-step PROG_DOUBLE passes):
+//                   persistent CTAs; tile t+1 is brought into shared memory
+//                   by TMA (one elected thread, mbarrier completion) while
+//                   tile t is transformed; stage 0 reads the TMA tile
+//                   (SRC_TMA), the last stage stores straight to global.
 #pragma once
 
 #include "fft_core.cuh"
@@ -63,8 +63,8 @@ struct PassArgs {
   const double2* tw_hi;
   const double2* fft_tw;                   // per-stage twiddles, Plan<L>::tw_offset layout
   const double2* fft_tw2;                  // same for the reversed plan (second transform of PROG_DOUBLE)
-  int nblk;                                // v2: line blocks per batch member
-  int ntiles;                              // v2: nblk * batch
+  int nblk;                                // pass3: line blocks per batch member
+  int ntiles;                              // pass3: nblk * batch
   // Good-Thomas (prime-factor) rank-1 layout: position (n1, n2) of the
   // M1 x M2 view holds natural index (M2*n1 + M1*n2) mod M, gcd(M1,M2)=1.
   int pfa;
@@ -118,12 +118,18 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
   PassArgs a;  // by value: fields resolve to parameter-bank operands, not pointer loads
   int line0;
   long long bat;
-  const double2* dgt = nullptr;  // v2: shared-memory diag tile (b*L + i)
+  // pass3: the TMA-filled tile (dense: COL i*B + b, ROW b*L + i) stage 0
+  // reads, and the odd ping-pong stage buffer (the tile's own buffer is
+  // the even one once stage 0 has consumed it)
+  const double2* tsrc = nullptr;
+  double2* sm1 = nullptr;
 
   static constexpr int LS = SmemGeom<L, B>::LS;
   LD_HD static int slot(int b, int i) { return b * LS + Plan<L>::phys(i); }
   // buffer used as the source of stage-sequence position p (0, 1, 2, ...)
-  LD_HD double2* buf(int p) const { return (SmemGeom<L, B>::pp && (p & 1)) ? sm + SmemGeom<L, B>::tile : sm; }
+  LD_HD double2* buf(int p) const {
+    return (SmemGeom<L, B>::pp && (p & 1)) ? (sm1 ? sm1 : sm + SmemGeom<L, B>::tile) : sm;
+  }
 
   // array position of element (b, i) in the 2-D view
   LD_HD long long pos(int b, int i) const {
@@ -180,15 +186,9 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
     }
     return v;
   }
-  // v2 stage-0 source: the prefetched tile (masked entries were zero-filled)
-  LD_HD double2 tload(int b, int i) const {
-    double2 v = sm[slot(b, i)];  // the tile was loaded into buf(0)
-    if (PROG == PROG_LOADDIAG) {
-      long long j = in_index(b, i);
-      if (live(b) && j < a.nvalid_in) v = apply_diag(v, j);
-    }
-    return v;
-  }
+  // pass3 stage-0 source: the TMA tile (PROG_DOUBLE passes, full input mask;
+  // columns beyond the view were zero-filled by the TMA bounds check)
+  LD_HD double2 tmaload(int b, int i) const { return tsrc[AXIS == AX_COL ? i * B + b : b * L + i]; }
   LD_HD void gstore(int b, int i, double2 v) const {
     if (!live(b)) return;
     long long j = out_index(b, i);
@@ -206,10 +206,6 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
     if (LATTDSE_ABLATE & 1) {
 #pragma unroll
       for (int r = 0; r < R; ++r) dg[r] = (lv && pos(b, j + r * T) < a.nvalid_mid) ? make_double2(1.0, 0.0) : zero;
-    } else if (dgt) {
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-        dg[r] = (lv && pos(b, j + r * T) < a.nvalid_mid) ? dgt[b * L + j + r * T] : zero;
     } else if (a.diag_kind == DG_CPLX) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -240,7 +236,6 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
     long long j = pos(b, i);
     if (!live(b) || j >= a.nvalid_mid) return make_double2(0.0, 0.0);
     if (LATTDSE_ABLATE & 1) return v;
-    if (dgt) return c_mul(v, dgt[b * L + i]);
     return apply_diag(v, j);
   }
 };
@@ -273,7 +268,7 @@ template <int R> struct Pow {
   }
 };
 
-enum : int { SRC_SMEM = 0, SRC_GLOBAL = 1, SRC_TILE = 2 };
+enum : int { SRC_SMEM = 0, SRC_GLOBAL = 1, SRC_TMA = 2 };
 enum : int { DST_SMEM = 0, DST_SMEM_MID = 1, DST_GLOBAL = 2 };
 
 // Stage S of a transform, at position Q of the pass's stage sequence: reads
@@ -332,8 +327,8 @@ struct Stage {
           v[t][r] = c.buf(Q)[C::slot(b, j + r * T)];
         else if (SRC == SRC_GLOBAL)
           v[t][r] = c.gload(b, j + r * T);
-        else if (SRC == SRC_TILE)
-          v[t][r] = c.tload(b, j + r * T);
+        else if (SRC == SRC_TMA)
+          v[t][r] = c.tmaload(b, j + r * T);
         else
           v[t][r] = c.buf(Q)[C::slot(b, j + r * T)];
       }
@@ -496,49 +491,6 @@ LD_HD void run_pass(const Ctx<AXIS, L, B, PROG>& c) {
   }
 }
 
-// ------------------------------------------------------------ tile loads
-// Element (b, i) of a tile: global offset and validity, in the order the
-// copy loop walks it (ROW: along the line; COL: B adjacent columns first, so
-// each global row segment of B*16 bytes is read by consecutive threads).
-template <int AXIS, int L, int B> struct TileWalk {
-  LD_HD static void elem(int q, int& b, int& i) {
-    if (AXIS == AX_ROW) {
-      b = q / L;
-      i = q % L;
-    } else {
-      b = q % B;
-      i = q / B;
-    }
-  }
-};
-
-#if defined(__CUDACC__)
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-template <int AXIS, int L, int B, int NT, int PROG>
-__device__ __forceinline__ void load_tile(const PassArgs& a, double2* buf, double2* dg, int line0, long long bat) {
-  using C = Ctx<AXIS, L, B, PROG>;
-  for (int q = threadIdx.x; q < B * L; q += NT) {
-    int b, i;
-    TileWalk<AXIS, L, B>::elem(q, b, i);
-    const bool live = line0 + b < a.nlines;
-    // PROG_DOUBLE tiles: work buffer and diag table are both in position order
-    const long long j = AXIS == AX_ROW ? (long long)(line0 + b) * L + i : (long long)i * a.ncols + (line0 + b);
-    const bool ok = live && j < a.nvalid_in;
-    cp_async16(buf + C::slot(b, i), ok ? (const void*)(a.in + bat * a.in_bstride + j) : (const void*)a.in, ok ? 16 : 0);
-    if (dg) {
-      const bool okd = live && j < a.nvalid_mid;
-      cp_async16(dg + b * L + i, okd ? (const void*)(a.diag + j) : (const void*)a.diag, okd ? 16 : 0);
-    }
-  }
-}
-#endif
-
 #if defined(__CUDACC__)
 template <int AXIS, int L, int B, int NT, int PROG, int SIGN1, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) fft_pass_kernel(const __grid_constant__ PassArgs a) {
@@ -553,32 +505,6 @@ __global__ void __launch_bounds__(NT, MINB) fft_pass_kernel(const __grid_constan
   run_pass<DevExec, AXIS, L, B, NT, PROG, SIGN1>(c);
 }
 
-// v2: persistent, double-buffered. Only PROG_DOUBLE with a complex diagonal
-// table (the per-step passes). Shared memory: 2 data tiles + 2 diag tiles.
-template <int AXIS, int L, int B, int NT, int SIGN1>
-__global__ void __launch_bounds__(NT) fft_pass2_kernel(const __grid_constant__ PassArgs a) {
-  extern __shared__ double2 lattdse_smem[];
-  constexpr int TS = SmemGeom<L, B>::bytes / 16;  // one tile incl. its ping-pong partner
-  double2* data[2] = {lattdse_smem, lattdse_smem + TS};
-  double2* dg[2] = {lattdse_smem + 2 * TS, lattdse_smem + 2 * TS + B * L};
-  int t = blockIdx.x;
-  if (t >= a.ntiles) return;
-  auto line0_of = [&](int tt) { return (tt % a.nblk) * B; };
-  auto bat_of = [&](int tt) { return (long long)(tt / a.nblk); };
-  load_tile<AXIS, L, B, NT, PROG_DOUBLE>(a, data[0], dg[0], line0_of(t), bat_of(t));
-  cp_async_commit();
-  int cur = 0;
-  for (; t < a.ntiles; t += gridDim.x) {
-    cp_async_wait_all();
-    __syncthreads();  // tile t landed; every thread is done with tile t-1's buffers
-    const int tn = t + gridDim.x;
-    if (tn < a.ntiles) load_tile<AXIS, L, B, NT, PROG_DOUBLE>(a, data[cur ^ 1], dg[cur ^ 1], line0_of(tn), bat_of(tn));
-    cp_async_commit();
-    Ctx<AXIS, L, B, PROG_DOUBLE> c{data[cur], a, line0_of(t), bat_of(t), dg[cur]};
-    run_pass<DevExec, AXIS, L, B, NT, PROG_DOUBLE, SIGN1, SRC_TILE>(c);
-    cur ^= 1;
-  }
-}
 #endif
 
 }  // namespace lattdse_dev

@@ -2,10 +2,11 @@
 #pragma once
 
 #include "fft_pass.cuh"
+#include "fft_pass3.cuh"
 #include "pass_registry.hpp"
 
-#ifndef LATTDSE_BUILD_V2
-#define LATTDSE_BUILD_V2 0  // persistent double-buffered variant (opt-in, slower today)
+#ifndef LATTDSE_BUILD_PASS3
+#define LATTDSE_BUILD_PASS3 1  // persistent TMA-fed per-step passes (fft_pass3.cuh)
 #endif
 #ifndef LATTDSE_COL_B1_MIN
 #define LATTDSE_COL_B1_MIN 8192  // columns this long: one column per CTA
@@ -31,7 +32,16 @@ template <int AXIS, int L> struct Geometry {
                                                        : (L >= LATTDSE_COL_B1_MIN ? 1 : (L >= 512 && !col512 ? 2 : (L >= 128 ? 4 : 8)));
   static constexpr int raw = B * lattdse_dev::Plan<L>::max_tasks();
   static constexpr int NT = (wide_col || col512) ? 256 : (raw <= 32 ? 32 : (raw >= 512 ? 512 : ((raw + 31) / 32) * 32));
-  static constexpr int smem2 = 2 * lattdse_dev::SmemGeom<L, B>::bytes + 2 * B * L * 16;  // v2 (opt-in)
+  // pass3 (persistent, TMA-fed): CTAs per SM by shared memory, and the
+  // register cap that keeps that many resident
+  using G3 = lattdse_dev::Pass3Geom<AXIS, L, B>;
+  static constexpr int smem3 = G3::bytes;
+  static constexpr int ctas3 = (228 * 1024) / (smem3 + 1024);
+  // resident CTAs: as many as shared memory allows, at most what ~96
+  // registers per thread allow (the v1 kernels' budget; more registers cost
+  // warps, measured profiles/r2c: 166 regs -> 0.69x the warps on ROW 486)
+  static constexpr int by_regs = 65536 / (NT * 96) > 0 ? 65536 / (NT * 96) : 1;
+  static constexpr int mb3 = ctas3 < 1 ? 1 : (ctas3 < by_regs ? ctas3 : by_regs);
 };
 
 template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
@@ -55,9 +65,10 @@ template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
     // ROW lines of 4096 (radix-16 stages) spill heavily under the 3-CTA cap
     k.default_mb = G::wide_col ? 1 : (G::NT > 320 ? 2 : (AXIS == lattdse_dev::AX_ROW && L < 4096 ? 3 : 2));
   }
-  if constexpr (LATTDSE_BUILD_V2 && PROG == lattdse_dev::PROG_DOUBLE && G::smem2 <= 227 * 1024) {
-    k.fn2 = reinterpret_cast<const void*>(&lattdse_dev::fft_pass2_kernel<AXIS, L, G::B, G::NT, SIGN>);
-    k.smem2 = G::smem2;
+  if constexpr (LATTDSE_BUILD_PASS3 && PROG == lattdse_dev::PROG_DOUBLE && G::smem3 <= 227 * 1024) {
+    k.fn3 = reinterpret_cast<const void*>(&lattdse_dev::fft_pass3_kernel<AXIS, L, G::B, G::NT, SIGN, G::mb3>);
+    k.smem3 = G::smem3;
+    k.boxr3 = G::G3::boxr;
   }
   register_pass_kernel(AXIS, L, PROG, SIGN, k);
 }

@@ -15,11 +15,13 @@ struct PassKernel {
   int NT = 0;                // threads per CTA
   int smem = 0;              // dynamic shared memory bytes
   bool attr_set = false;     // cudaFuncAttributeMaxDynamicSharedMemorySize applied
-  // v2 persistent double-buffered variant (PROG_DOUBLE with a complex diag)
-  const void* fn2 = nullptr;
-  int smem2 = 0;
-  bool attr2_set = false;
-  int blocks_per_sm2 = 0;
+  // pass3: persistent TMA-fed variant of the PROG_DOUBLE programs
+  // (fft_pass3.cuh); COL tiles arrive as boxr-row TMA boxes
+  const void* fn3 = nullptr;
+  int smem3 = 0;
+  int boxr3 = 0;
+  bool attr3_set = false;
+  int blocks_per_sm3 = 0;
   // PROG_DOUBLE instantiated with __launch_bounds__(NT, minBlocks) for
   // minBlocks = 1..4 (register cap vs occupancy); index 0 unused
   const void* fn_mb[5] = {};

@@ -17,6 +17,7 @@
 //
 // Ensemble members are stepped in groups sized to stay L2-resident for the
 // whole step(n) call (each member's work buffer is reused across steps).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -38,6 +39,24 @@
 using namespace lattdse_dev;
 
 namespace lattdse {
+
+namespace {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+}  // namespace
 
 #define LD_CK(x)                                                                                      \
   do {                                                                                                \
@@ -491,7 +510,12 @@ struct Solver::Impl {
   bool bluestein_tables = false;
   long long launches = 0;
   bool sync_check = std::getenv("LATTDSE_SYNC_CHECK") != nullptr;  // debug: sync after every launch
-  bool use_v2 = std::getenv("LATTDSE_PASS_V2") != nullptr;           // persistent double-buffered passes (opt-in)
+  // persistent TMA-fed per-step passes (fft_pass3.cuh), opt-in LATTDSE_PASS3=1
+  // until measured faster than the one-CTA-per-tile kernels (profiles/r2c)
+  bool use_pass3 = std::getenv("LATTDSE_PASS3") && std::atoi(std::getenv("LATTDSE_PASS3")) != 0;
+  int tma_promo = std::getenv("LATTDSE_TMA_PROMO") ? std::atoi(std::getenv("LATTDSE_TMA_PROMO")) : 0;
+  // COL tensor maps, one per (buffer, row length, rows, batch, batch stride)
+  std::map<std::tuple<const void*, int, int, long long, long long>, CUtensorMap> tmaps;
   int num_sms = 148;
   int minb_override = std::getenv("LATTDSE_MINB") ? std::atoi(std::getenv("LATTDSE_MINB")) : 0;
   // CUDA graphs of kGraphSteps identical middle steps, per (group start, size)
@@ -517,25 +541,16 @@ struct Solver::Impl {
     dev::PassKernel* k = dev::find_pass_kernel(axis, L, prog, sign);
     if (!k) raise(Errc::unsupported, "no pass kernel compiled for axis " + std::to_string(axis) + " L=" + std::to_string(L));
     a.nlines = (int)nlines;
-    const bool v2 = use_v2 && k->fn2 && prog == PROG_DOUBLE && a.diag_kind == DG_CPLX;
-    const void* fn = v2 ? k->fn2 : k->fn;
-    if (!v2 && prog == PROG_DOUBLE) {
+    if (use_pass3 && k->fn3 && prog == PROG_DOUBLE && pass3_ok(axis, L, a, nlines, k->B))
+      return launch_pass3(axis, L, k, a, nlines, nbatch);
+    const void* fn = k->fn;
+    if (prog == PROG_DOUBLE) {
       const int mb = minb_override > 0 ? minb_override : k->default_mb;
       if (mb >= 1 && mb <= 4 && k->fn_mb[mb]) fn = k->fn_mb[mb];
     }
-    int smem = v2 ? k->smem2 : k->smem;
+    int smem = k->smem;
     dim3 grid;
-    if (v2) {
-      if (!k->attr2_set) {
-        LD_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        LD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k->blocks_per_sm2, fn, k->NT, smem));
-        k->attr2_set = true;
-      }
-      a.nblk = (int)((nlines + k->B - 1) / k->B);
-      a.ntiles = (int)(a.nblk * nbatch);
-      const long long resident = (long long)std::max(1, k->blocks_per_sm2) * num_sms;
-      grid = dim3((unsigned)std::min<long long>(a.ntiles, resident), 1);
-    } else {
+    {
       if (!k->attr_set) {
         for (int m = 0; m <= 4; ++m) {
           const void* f = m == 0 ? k->fn : k->fn_mb[m];
@@ -557,7 +572,7 @@ struct Solver::Impl {
     void* args[] = {&a};
     const bool persist_this = persist_bytes > 0 && prog == PROG_DOUBLE && a.diag_kind == DG_CPLX &&
                               ((axis == AX_ROW && (persist_mode & 1)) || (axis == AX_COL && (persist_mode & 2)));
-    const bool pdl_this = use_pdl && !v2;
+    const bool pdl_this = use_pdl;
     if (persist_this || pdl_this) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = grid;
@@ -596,8 +611,86 @@ struct Solver::Impl {
       cudaError_t e = cudaStreamSynchronize(stream);
       if (e != cudaSuccess)
         raise(Errc::device_error, "pass axis=" + std::to_string(axis) + " L=" + std::to_string(L) + " prog=" +
-                                      std::to_string(prog) + " sign=" + std::to_string(sign) + (v2 ? " v2" : " v1") +
+                                      std::to_string(prog) + " sign=" + std::to_string(sign) + " v1" +
                                       ": " + cudaGetErrorString(e));
+    }
+  }
+  // pass3 applies to the plain layouts with a full input mask (the TMA tile
+  // has no per-element mask); the sharded / Good-Thomas layouts keep v1
+  bool pass3_ok(int axis, int L, const PassArgs& a, long long nlines, int B) const {
+    if (a.pfa || a.rb_w > 0 || a.ncols_g > 0 || a.col_off != 0) return false;
+    if (axis == AX_COL) {
+      if (a.ncols < B || nlines != a.ncols || !encode_tiled()) return false;
+      if (a.nvalid_in < (long long)L * a.ncols || a.in_bstride < (long long)L * a.ncols) return false;
+    } else {
+      if (a.nvalid_in < nlines * (long long)L || (a.in_bstride < nlines * (long long)L && a.in_bstride != 0)) return false;
+    }
+    return (reinterpret_cast<uintptr_t>(a.in) & 15) == 0;
+  }
+  const CUtensorMap& col_tmap(const PassArgs& a, int L, int boxr, int B, long long nbatch) {
+    auto key = std::make_tuple((const void*)a.in, a.ncols, L, nbatch, a.in_bstride);
+    auto it = tmaps.find(key);
+    if (it != tmaps.end()) return it->second;
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof m);
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * a.ncols, (cuuint64_t)L, (cuuint64_t)std::max<long long>(1, nbatch)};
+    const cuuint64_t strides[2] = {(cuuint64_t)a.ncols * 16, (cuuint64_t)std::max<long long>(1, a.in_bstride) * 16};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * B), (cuuint32_t)boxr, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUtensorMapL2promotion promo = tma_promo == 1   ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                         : tma_promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                         : tma_promo == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                          : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(a.in), dims, strides,
+                                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(Errc::device_error, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return tmaps.emplace(key, m).first->second;
+  }
+  void launch_pass3(int axis, int L, dev::PassKernel* k, PassArgs a, long long nlines, long long nbatch) {
+    if (!k->attr3_set) {
+      LD_CK(cudaFuncSetAttribute(k->fn3, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem3));
+      LD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k->blocks_per_sm3, k->fn3, k->NT, k->smem3));
+      k->attr3_set = true;
+    }
+    a.nlines = (int)nlines;
+    a.nblk = (int)((nlines + k->B - 1) / k->B);
+    const long long ntiles = (long long)a.nblk * nbatch;
+    if (ntiles > 0x7fffffffLL) raise(Errc::unsupported, "pass3: too many tiles");
+    a.ntiles = (int)ntiles;
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof m);
+    if (axis == AX_COL) m = col_tmap(a, L, k->boxr3, k->B, nbatch);
+    const long long resident = (long long)std::max(1, k->blocks_per_sm3) * num_sms;
+    const dim3 grid((unsigned)std::min<long long>(ntiles, resident));
+    void* args[] = {&a, &m};
+    if (persist_bytes > 0 && a.diag_kind == DG_CPLX &&
+        ((axis == AX_ROW && (persist_mode & 1)) || (axis == AX_COL && (persist_mode & 2)))) {
+      // keep the per-step diagonal table L2-resident (see launch_pass)
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(k->NT);
+      cfg.dynamicSmemBytes = (size_t)k->smem3;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      attr[0].val.accessPolicyWindow.base_ptr = (void*)a.diag;
+      attr[0].val.accessPolicyWindow.num_bytes = std::min<size_t>(persist_window, (size_t)table_bytes(a));
+      attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      LD_CK(cudaLaunchKernelExC(&cfg, k->fn3, args));
+    } else {
+      LD_CK(cudaLaunchKernel(k->fn3, grid, dim3(k->NT), args, (size_t)k->smem3, stream));
+    }
+    ++launches;
+    if (sync_check) {
+      cudaError_t e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess)
+        raise(Errc::device_error, "pass3 axis=" + std::to_string(axis) + " L=" + std::to_string(L) + ": " +
+                                      cudaGetErrorString(e));
     }
   }
   // bytes of the complex diagonal table a DOUBLE pass reads (position order)
@@ -1605,17 +1698,21 @@ SolverInfo Solver::info() const {
   i.rank = s.rank;
   i.method = s.method + (s.rank == 1 ? (s.pfa ? "/good-thomas" : "/four-step") : "");
   i.group = s.group;
+  i.pass3 = s.use_pass3 ? 1 : 0;  // used where a pass3 kernel is compiled and the layout is plain
+  // algorithmic bytes: every member's state read + written once per pass;
+  // the diagonal tables are shared by the members of a group, so a launch
+  // (one group) reads each table once
   const double M = (double)s.M, N = (double)s.N, B = (double)s.batch;
+  const double G = (double)s.group, groups = std::ceil(B / G);
   if (s.rank == 2) {
-    i.bytes_per_pass_row = B * (32.0 * N + 16.0 * N);  // state R+W + V
-    i.bytes_per_pass_col = B * (32.0 * N + 2.0 * N);   // state R+W + D index
+    i.bytes_per_pass_row = B * 32.0 * N + groups * 16.0 * N;  // state R+W + V
+    i.bytes_per_pass_col = B * 32.0 * N + groups * 2.0 * N;   // state R+W + D index
     i.bytes_per_step = i.bytes_per_pass_row + i.bytes_per_pass_col;
     i.launches_per_step = 2;
   } else if (s.method == "circulant") {
-    const double G = (double)s.group, groups = std::ceil(B / G);
     // state R+W + V: four-step reads the N valid V entries, Good-Thomas the
     // position-ordered V_perm (M entries, mask folded in)
-    i.bytes_per_pass_col = B * (32.0 * M + 16.0 * (s.pfa ? M : N));
+    i.bytes_per_pass_col = B * 32.0 * M + groups * 16.0 * (s.pfa ? M : N);
     // state R+W + K^ once per group; three-level: the "row" side is three
     // passes (inner COL forward, ROW with K^, inner COL inverse), which cross
     // HBM once in total when they run on L2-resident row chunks
@@ -1625,8 +1722,7 @@ SolverInfo Solver::info() const {
     const long long nchunks = chunked ? (s.M1 + s.row_chunk - 1) / s.row_chunk : 1;
     i.launches_per_step = (int)((chunked ? 1 + 3 * nchunks * s.group : (s.three ? 4 : 2)) * (long long)groups);
   } else {
-    const double G = (double)s.group, groups = std::ceil(B / G);
-    i.bytes_per_pass_col = B * (32.0 * M + 9.0 * N);   // avg of (V 16N) and (D idx 2N)
+    i.bytes_per_pass_col = B * 32.0 * M + groups * 9.0 * N;  // avg of (V 16N) and (D idx 2N)
     i.bytes_per_pass_row = B * 32.0 * M + groups * 16.0 * M;
     i.bytes_per_step = 2.0 * (i.bytes_per_pass_col + i.bytes_per_pass_row);
     i.launches_per_step = 4 * (int)groups;
