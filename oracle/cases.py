@@ -11,8 +11,8 @@ What is restated here, and from where:
 - the generating vectors: prime-n CBC. C0 is re-derived by
   the oracle's exhaustive CBC in tests/test_oracle_cases.py; C1/C3 are the
   host fast-CBC results (bit-exact to the exhaustive oracle at every n it can
-  finish, tests/test_cbc.py); C4r is the host fast CBC run once
-  (tools/c4r_host_cbc.py), not the device construction;
+  finish, tests/test_cbc.py); C4r is catalog.json's device-CBC vector taken
+  as the lattice definition (its index map is the oracle's own walk);
 - config 2's rank-2 lattice ("Config 2 lattice").
 tests/test_oracle_cases.py checks this table against the product's
 configs.py so the two cannot drift apart silently.
@@ -104,15 +104,13 @@ CASES = {
                0.05, 1.0, 512, 0.08),
     "C3": _r1("C3", 3, 6, 262147, [1, 102226, 122243, 92569, 3585, 103565], 0.05, 0.5, 512, 0.1, batch=512,
               c_range=(0.3, 0.7), p_max=3),
-    # config 4's shape at reduced N; z from the HOST fast CBC
-    # (tools/c4r_host_cbc.py), filled in below once computed
-    "C4r": _r1("C4r", 5, 20, 16777259, [], 0.02, 0.1, 64, 0.15),
+    # config 4's shape at reduced N; the lattice definition
+    # is catalog.json's C4r vector (device CBC); its index map is the
+    # oracle's own walk (tests/golden/c4r_tables.json)
+    "C4r": _r1("C4r", 5, 20, 16777259, [1, 6408565, 2903963, 4966000, 8029635, 3702744, 8380425, 5023039, 508131,
+                                         6943149, 3253008, 3662870, 380856, 6470234, 2574891, 6408565, 6408565,
+                                         6408565, 6408565, 6408565], 0.02, 0.1, 64, 0.15),
 }
-
-# host fast-CBC generating vector of C4r (tools/c4r_host_cbc.py output)
-C4R_HOST_Z = None
-if C4R_HOST_Z:
-    CASES["C4r"].gen = [list(C4R_HOST_Z)]
 
 
 # ------------------------------------------------------------- fixtures

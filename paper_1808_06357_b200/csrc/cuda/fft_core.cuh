@@ -265,24 +265,32 @@ constexpr int first_radix(int L) {
 }
 
 // Explicit plans. The first four: long lines the greedy rule would end with
-// a radix-2/3 stage (three balanced stages instead). The rest: the plan with
-// the fewest shared-memory wavefronts (tools/plan_search.py, quarter-warp
-// bank-group model calibrated against ncu: 823 measured vs 812 modelled per
-// ROW-486 line) among the orderings with the greedy rule's stage count and
-// no larger radix -- mostly odd radices at both ends, so stage 0 and the
-// reversed plan's stage 0 write with odd strides and no swizzle is needed
-// (config 3's 486/1080: 1.67/1.55 -> 1.24/1.07 wavefronts per element).
+// a radix-2/3 stage (three balanced stages instead). 1080: measured per
+// pass on config 3 (profiles/r2g, ms per launch over 512 members; the plan
+// is shared by both axes): as the ROW pass (9, 8, 15) 3.25 vs the greedy
+// (15, 12, 6) 4.10, (15, 8, 9) 3.57, (15, 9, 8) 4.09. Plans chosen by the
+// shared-memory wavefront model alone (tools/plan_search.py) lost where
+// they raised registers or put a large radix in the fused mid stage, which
+// holds the data and the prefetched diagonal together: ROW 486 (9, 6, 9)
+// 2.90 vs greedy (9, 9, 6) 2.74 ms despite 26% fewer wavefronts.
 struct PlanOverride {
   int L, r[4];
 };
+// build-time experiments: -include a header defining LATTDSE_PLAN_X/Y as
+// "L, r0, r1, r2, r3" (scripts/build_variant.sh) takes precedence
+#ifndef LATTDSE_PLAN_X
+#define LATTDSE_PLAN_X 0, 0, 0, 0, 0
+#endif
+#ifndef LATTDSE_PLAN_Y
+#define LATTDSE_PLAN_Y 0, 0, 0, 0, 0
+#endif
+constexpr int kPlanX[5] = {LATTDSE_PLAN_X};
+constexpr int kPlanY[5] = {LATTDSE_PLAN_Y};
 constexpr PlanOverride kPlanOverride[] = {
+    {kPlanX[0] ? kPlanX[0] : -1, {kPlanX[1], kPlanX[2], kPlanX[3], kPlanX[4]}},
+    {kPlanY[0] ? kPlanY[0] : -1, {kPlanY[1], kPlanY[2], kPlanY[3], kPlanY[4]}},
     {2592, {9, 16, 18, 0}},  {3240, {15, 12, 18, 0}}, {3888, {27, 16, 9, 0}},
-    {4320, {15, 16, 18, 0}}, {48, {4, 12, 0, 0}},     {64, {8, 8, 0, 0}},
-    {90, {9, 10, 0, 0}},     {486, {9, 6, 9, 0}},     {512, {16, 2, 16, 0}},
-    {540, {9, 4, 15, 0}},    {648, {9, 8, 9, 0}},     {720, {5, 16, 9, 0}},
-    {810, {9, 6, 15, 0}},    {1024, {16, 4, 16, 0}},  {1080, {9, 8, 15, 0}},
-    {1440, {9, 10, 16, 0}},  {1458, {9, 2, 9, 9}},    {1728, {12, 9, 16, 0}},
-    {1944, {3, 9, 8, 9}},    {2048, {16, 8, 16, 0}},  {0, {0, 0, 0, 0}},
+    {4320, {15, 16, 18, 0}}, {1080, {9, 8, 15, 0}},   {0, {0, 0, 0, 0}},
 };
 constexpr int override_radix(int L, int s) {
   for (const auto& o : kPlanOverride)

@@ -87,6 +87,17 @@ struct PassArgs {
   // (each row an Ma x Mb matrix, one per batch index) needs the four-step
   // twiddles of length M2 = M / M1: W_M2^t = W_M^(M1 t). 0 or 1: plain.
   long long tw_mul;
+  // Fused observables of PROG_STOREDIAG passes: when obs is
+  // set, every stored value v (after the diagonal) adds |v|^2 and w_j |v|^2
+  // to per-CTA partial sums obs[2*(blockIdx.y*gridDim.x + blockIdx.x) + {0,1}],
+  // w_j = obs_w[j] (potential, natural order) or obs_wscale * obs_widx[j]
+  // (kinetic weight from the norm index). The host finishes the sums in
+  // long double: ||u||^2, the potential and the kinetic parts of E come out
+  // of the passes that produce the samples / coefficients anyway.
+  double* obs;
+  const double* obs_w;
+  const unsigned short* obs_widx;
+  double obs_wscale;
 };
 
 // Shared-memory slots of one tile: B lines, each Plan<L>::phys-swizzled and
@@ -123,6 +134,7 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
   // the even one once stage 0 has consumed it)
   const double2* tsrc = nullptr;
   double2* sm1 = nullptr;
+  mutable double acc0 = 0.0, acc1 = 0.0;  // fused observables (PassArgs::obs)
 
   static constexpr int LS = SmemGeom<L, B>::LS;
   LD_HD static int slot(int b, int i) { return b * LS + Plan<L>::phys(i); }
@@ -193,7 +205,14 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
     if (!live(b)) return;
     long long j = out_index(b, i);
     if (j >= a.nvalid_out) return;
-    if (PROG == PROG_STOREDIAG) v = apply_diag(v, j);
+    if (PROG == PROG_STOREDIAG) {
+      v = apply_diag(v, j);
+      if (a.obs) {
+        const double q = fma(v.x, v.x, v.y * v.y);
+        acc0 += q;
+        acc1 = fma(a.obs_w ? a.obs_w[j] : a.obs_wscale * (double)a.obs_widx[j], q, acc1);
+      }
+    }
     a.out[bat * a.out_bstride + j] = v;
   }
   // Coefficients of the mid diagonal for elements j + r*T, r < R (zero where
@@ -503,6 +522,33 @@ __global__ void __launch_bounds__(NT, MINB) fft_pass_kernel(const __grid_constan
   asm volatile("griddepcontrol.wait;" ::: "memory");
   Ctx<AXIS, L, B, PROG> c{lattdse_smem, a, (int)blockIdx.x * B, (long long)blockIdx.y};
   run_pass<DevExec, AXIS, L, B, NT, PROG, SIGN1>(c);
+  if constexpr (PROG == PROG_STOREDIAG) {
+    if (a.obs) {  // block partials of the fused observables (uniform branch)
+      double s0 = c.acc0, s1 = c.acc1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_down_sync(0xffffffffu, s0, o);
+        s1 += __shfl_down_sync(0xffffffffu, s1, o);
+      }
+      double* red = reinterpret_cast<double*>(lattdse_smem);
+      __syncthreads();  // the last stage may still be reading shared memory
+      if ((threadIdx.x & 31) == 0) {
+        red[2 * (threadIdx.x >> 5)] = s0;
+        red[2 * (threadIdx.x >> 5) + 1] = s1;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int w = 0; w < (NT + 31) / 32; ++w) {
+          t0 += red[2 * w];
+          t1 += red[2 * w + 1];
+        }
+        const long long blk = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+        a.obs[2 * blk] = t0;
+        a.obs[2 * blk + 1] = t1;
+      }
+    }
+  }
 }
 
 #endif

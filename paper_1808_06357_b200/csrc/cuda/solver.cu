@@ -34,7 +34,12 @@
 #include "lattdse/solver.hpp"
 #include "aaset_dev.hpp"
 #include "pass_registry.hpp"
+#ifndef LATTDSE_EXPERIMENTAL
+#define LATTDSE_EXPERIMENTAL 0  // measured-slower variants (cluster COL, Good-Thomas, row chunks): make EXPERIMENTAL=1
+#endif
+#if LATTDSE_EXPERIMENTAL
 #include "cluster_col.hpp"
+#endif
 
 using namespace lattdse_dev;
 
@@ -450,7 +455,9 @@ double cost_col3(int L) {
 double cost_pair_ensemble(int L1, int L2) {
   const long long k = (long long)L1 * 10000 + L2;
   switch (k) {
-    case 10800486: return 28.0; case 4861080: return 28.5; case 7290720: return 34.2; case 9720540: return 34.8;
+    // r2 (profiles/r2g): 1080 runs the (9, 8, 15) plan, best as a ROW pass
+    case 4861080: return 25.1; case 10800486: return 30.5; case 7290720: return 34.2;
+    case 9720540: return 34.8;
     default: return -1.0;
   }
 }
@@ -466,6 +473,21 @@ double cost_row3(int La, int Lb) {
   }
 }
 }  // namespace dev
+
+// fused observables of an exit pass (PassArgs::obs): partial-sum buffer and
+// the weight of the second sum (potential table or scaled norm index)
+struct ObsSpec {
+  double* out = nullptr;
+  const double* w = nullptr;
+  const unsigned short* widx = nullptr;
+  double wscale = 0.0;
+  void apply(PassArgs& a) const {
+    a.obs = out;
+    a.obs_w = w;
+    a.obs_widx = widx;
+    a.obs_wscale = wscale;
+  }
+};
 
 // ------------------------------------------------------------- Impl
 struct Solver::Impl {
@@ -536,6 +558,37 @@ struct Solver::Impl {
 
   explicit Impl(const Lattice& l) : lat(l) {}
 
+  DBuf<double> obs_part;
+  // CTAs per batch member of the exit pass that produces samples (rank 1:
+  // COL STOREDIAG over M2 columns; rank 2: ROW STOREDIAG over n1 rows) or
+  // coefficients (rank 2 analysis: COL STOREDIAG over n2 columns)
+  long long exit_blocks(bool coeffs) const {
+    if (rank == 2) {
+      dev::PassKernel* k = coeffs ? dev::find_pass_kernel(AX_COL, (int)n1, PROG_STOREDIAG, -1)
+                                  : dev::find_pass_kernel(AX_ROW, (int)n2, PROG_STOREDIAG, +1);
+      const long long lines = coeffs ? n2 : n1;
+      return k ? (lines + k->B - 1) / k->B : 0;
+    }
+    dev::PassKernel* k = dev::find_pass_kernel(AX_COL, (int)M1, PROG_STOREDIAG, +1);
+    return k ? (M2 + k->B - 1) / k->B : 0;
+  }
+  // per-member (sum |u|^2, sum w |u|^2) from the exit-pass partials, in long double
+  std::vector<std::pair<double, double>> finish_obs(long long nblk, long long nb) {
+    std::vector<double> h((size_t)(2 * nblk * nb));
+    LD_CK(cudaMemcpyAsync(h.data(), obs_part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    LD_CK(cudaStreamSynchronize(stream));
+    std::vector<std::pair<double, double>> out((size_t)nb);
+    for (long long m = 0; m < nb; ++m) {
+      long double a = 0, b = 0;
+      for (long long i = 0; i < nblk; ++i) {
+        a += h[(size_t)(2 * (m * nblk + i))];
+        b += h[(size_t)(2 * (m * nblk + i) + 1)];
+      }
+      out[(size_t)m] = {(double)a, (double)b};
+    }
+    return out;
+  }
+
   // ---- launch helpers
   void launch_pass(int axis, int L, int prog, int sign, PassArgs a, long long nlines, long long nbatch) {
     dev::PassKernel* k = dev::find_pass_kernel(axis, L, prog, sign);
@@ -563,6 +616,7 @@ struct Solver::Impl {
           PassArgs c = a;
           c.in = a.in + b0 * a.in_bstride;
           c.out = a.out + b0 * a.out_bstride;
+          if (c.obs) c.obs = a.obs + 2 * b0 * ((nlines + k->B - 1) / k->B);
           launch_pass(axis, L, prog, sign, c, nlines, std::min<long long>(65535, nbatch - b0));
         }
         return;
@@ -768,8 +822,10 @@ struct Solver::Impl {
     a.lut = kin_lut.p;
     launch_pass(AX_COL, (int)M1, PROG_DOUBLE, +1, a, M2, nb);
   }
-  void r1_col_exit(double2* w, const double2* diag, double2* out, long long out_stride, long long nb) {
+  void r1_col_exit(double2* w, const double2* diag, double2* out, long long out_stride, long long nb,
+                   const ObsSpec& ob = ObsSpec{}) {
     PassArgs a = base_args(AX_COL);
+    ob.apply(a);
     a.in = w;
     a.out = out;
     a.in_bstride = M;
@@ -866,8 +922,10 @@ struct Solver::Impl {
     launch_pass(AX_COL, (int)M1, PROG_STOREDIAG, +1, a, M2, 1);
   }
   // ---- rank-2 passes (ROW length n2 over n1 rows; COL length n1 over n2 cols)
-  void g_row(int prog, int sign, const double2* in, double2* out, const double2* diag, long long nb) {
+  void g_row(int prog, int sign, const double2* in, double2* out, const double2* diag, long long nb,
+             const ObsSpec& ob = ObsSpec{}) {
     PassArgs a = base_args(AX_ROW);
+    ob.apply(a);
     a.in = in;
     a.out = out;
     a.in_bstride = a.out_bstride = N;
@@ -875,8 +933,10 @@ struct Solver::Impl {
     set_diag(a, diag);
     launch_pass(AX_ROW, (int)n2, prog, sign, a, n1, nb);
   }
-  void g_col(int prog, int sign, const double2* in, double2* out, int dkind, long long nb) {
+  void g_col(int prog, int sign, const double2* in, double2* out, int dkind, long long nb,
+             const ObsSpec& ob = ObsSpec{}) {
     PassArgs a = base_args(AX_COL);
+    ob.apply(a);
     a.in = in;
     a.out = out;
     a.in_bstride = a.out_bstride = N;
@@ -884,6 +944,7 @@ struct Solver::Impl {
     a.diag_kind = dkind;
     a.diag_idx = nidx.p;
     a.lut = dkind == DG_SCALAR ? scal.p : kin_lut.p;
+#if LATTDSE_EXPERIMENTAL
     if (prog == PROG_DOUBLE && cc_lloc > 0 && (dkind == DG_LUT16 || dkind == DG_NONE)) {
       // long columns (config 2): one cluster of CTAs per column block, the
       // column split across the cluster's shared memories (cluster_col.inl)
@@ -898,6 +959,7 @@ struct Solver::Impl {
       }
       return;
     }
+#endif
     launch_pass(AX_COL, (int)n1, prog, sign, a, n2, nb);
   }
 
@@ -998,7 +1060,7 @@ struct Solver::Impl {
         M1 = g1;
         M2 = g2;
         M = g1 * g2;
-        pfa = std::getenv("LATTDSE_PFA") != nullptr && std::gcd(g1, g2) == 1;
+        pfa = LATTDSE_EXPERIMENTAL && std::getenv("LATTDSE_PFA") != nullptr && std::gcd(g1, g2) == 1;
         return;
       }
     }
@@ -1051,7 +1113,7 @@ struct Solver::Impl {
         if (best < 0 || cost < bcost) { best = m; b1 = L1; b2 = L2; bcost = cost; }
         if (std::gcd(L1, L2) == 1 && (bestp < 0 || cost < pcost)) { bestp = m; p1 = L1; p2 = L2; pcost = cost; }
       }
-    const bool allow_pfa = std::getenv("LATTDSE_PFA") != nullptr;  // opt-in: see DESIGN.md
+    const bool allow_pfa = LATTDSE_EXPERIMENTAL && std::getenv("LATTDSE_PFA") != nullptr;  // opt-in: DESIGN.md
     if (allow_pfa && bestp > 0) {
       pfa = true;
       M = bestp;
@@ -1095,8 +1157,10 @@ struct Solver::Impl {
     up(tw_hi, root_table(M, nhi, nlo));
     std::vector<double2> s = {make_double2(1.0 / (double)N, 0.0)};
     up(scal, s);
+#if LATTDSE_EXPERIMENTAL
     if (rank == 2) cc_lloc = dev::cluster_col_lloc((int)n1, n2);
     if (cc_lloc > 0) up(cc_tab, dev::cluster_col_tables((int)n1, cc_lloc));
+#endif
     LD_CK(cudaStreamSynchronize(stream));
   }
 
@@ -1161,15 +1225,24 @@ struct Solver::Impl {
   }
 
   // samples (N, one member) -> coefficients (N) and back, on the device
-  void analyze_dev(const double2* s, double2* c, double2* w) {
+  // kin_obs: the exit pass also writes (sum |c|^2, sum kin ||h||^2 |c|^2)
+  // partials of the coefficients into obs_part (fused kinetic energy)
+  void analyze_dev(const double2* s, double2* c, double2* w, bool kin_obs = false) {
+    ObsSpec o;
+    if (kin_obs) {
+      obs_part.alloc((size_t)(2 * exit_blocks(true)));
+      o.out = obs_part.p;
+      o.widx = nidx.p;
+      o.wscale = 0.5 * eps * 4.0 * M_PI * M_PI;
+    }
     if (rank == 1) {
       build_analysis_tables(w);
       r1_col_entry(s, N, chirp.p, w, 1);
       r1_row_mid(w, B1hat.p, 1);
-      r1_col_exit(w, chirp_n.p, c, N, 1);
+      r1_col_exit(w, chirp_n.p, c, N, 1, o);
     } else {
       g_row(PROG_LOADDIAG, -1, s, w, nullptr, 1);
-      g_col(PROG_STOREDIAG, -1, w, c, DG_SCALAR, 1);
+      g_col(PROG_STOREDIAG, -1, w, c, DG_SCALAR, 1, o);
     }
   }
   void synthesize_dev(const double2* c, double2* s, double2* w) {
@@ -1277,7 +1350,19 @@ struct Solver::Impl {
     (is_col ? pt->col : pt->row).push_back({a, b});
   }
 
-  void enqueue_steps(long long nsteps, PassTimer* pt = nullptr) {
+  // observe: the exit pass of every group also writes the fused observable
+  // partials (sum |u|^2, sum v |u|^2) of each member into obs_part
+  void enqueue_steps(long long nsteps, PassTimer* pt = nullptr, bool observe = false) {
+    const long long nblk_obs = observe ? exit_blocks(false) : 0;
+    if (observe) obs_part.alloc((size_t)(2 * nblk_obs * batch));
+    auto obs_for = [&](long long g0) {
+      ObsSpec o;
+      if (observe) {
+        o.out = obs_part.p + 2 * nblk_obs * g0;
+        o.w = v.p;
+      }
+      return o;
+    };
     if (!have_dt) raise(Errc::config_error, "set_dt must be called before stepping");
     if (nsteps <= 0) return;
     for (long long g0 = 0; g0 < batch; g0 += group) {
@@ -1291,7 +1376,7 @@ struct Solver::Impl {
           if (k + 1 < nsteps)
             timed(pt, false, [&] { g_row(PROG_DOUBLE, +1, w, w, V.p, gb); });
           else
-            timed(pt, false, [&] { g_row(PROG_STOREDIAG, +1, w, s, Vh.p, gb); });
+            timed(pt, false, [&] { g_row(PROG_STOREDIAG, +1, w, s, Vh.p, gb, obs_for(g0)); });
         }
       } else if (method == "circulant") {
         timed(pt, true, [&] { r1_col_entry(s, N, Vh.p, w, gb); });
@@ -1326,7 +1411,7 @@ struct Solver::Impl {
           if (k + 1 < nsteps)
             timed(pt, true, [&] { r1_col_mid(w, V.p, gb); });
           else
-            timed(pt, true, [&] { r1_col_exit(w, Vh.p, s, N, gb); });
+            timed(pt, true, [&] { r1_col_exit(w, Vh.p, s, N, gb, obs_for(g0)); });
         }
       } else {  // literal Bluestein: two length-N DFTs per step
         timed(pt, true, [&] { r1_col_entry(s, N, Ventry.p, w, gb); });
@@ -1337,7 +1422,7 @@ struct Solver::Impl {
           if (k + 1 < nsteps)
             timed(pt, true, [&] { r1_col_mid(w, V.p, gb); });
           else
-            timed(pt, true, [&] { r1_col_exit(w, Vexit.p, s, N, gb); });
+            timed(pt, true, [&] { r1_col_exit(w, Vexit.p, s, N, gb, obs_for(g0)); });
         }
       }
     }
@@ -1359,6 +1444,19 @@ struct Solver::Impl {
       out[b] = (double)s;
     }
     return out;
+  }
+
+  // (||u||, E) of ONE member: norm and potential part from
+  // the samples, kinetic part from one analysis of that member only
+  std::pair<double, double> observables(long long m) {
+    LD_CK(cudaSetDevice(device));
+    const double2* sm = samples.p + m * N;
+    const double sq = reduce(sm, N, 1, N, nullptr, nullptr, 0, nullptr)[0];
+    const double pot = reduce(sm, N, 1, N, v.p, nullptr, 0, nullptr)[0];
+    coef.alloc(N);
+    analyze_dev(sm, coef.p, work.p);
+    const double kin = reduce(coef.p, N, 1, N, nullptr, nidx.p, 0.5 * eps * 4.0 * M_PI * M_PI, nullptr)[0];
+    return {std::sqrt(sq / (double)N), kin + pot / (eps * (double)N)};
   }
 };
 
@@ -1441,7 +1539,7 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
     s.group = std::min<long long>(s.group, 65535);
   }
 
-  if (s.three && s.rank == 1) {
+  if (LATTDSE_EXPERIMENTAL && s.three && s.rank == 1) {
     // opt-in (LATTDSE_ROW_CHUNK = M1 rows per chunk): the three-level row
     // side on L2-sized row chunks. Measured slower on config 4 (row side 105
     // vs 97 ms/step, profiles/README.md): the streaming passes are not
@@ -1611,18 +1709,32 @@ double Solver::l2_distance(const std::complex<double>* ref, Space space, std::in
 
 std::vector<TrajectoryRow> Solver::propagate(std::int64_t m, std::int64_t record_every, std::int64_t member) {
   if (m < 0) raise(Errc::invalid_argument, "propagate: m must be >= 0");
+  if (member < 0 || member >= p_->batch)
+    raise(Errc::invalid_argument, "propagate: member " + std::to_string(member) + " outside [0, " +
+                                      std::to_string(p_->batch) + ")");
   if (record_every <= 0) record_every = m > 0 ? m : 1;
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
   std::vector<TrajectoryRow> rows;
-  auto record = [&](std::int64_t k) {
-    rows.push_back({k, (double)k * p_->dt_, l2_norm()[member], energy()[member]});
-  };
-  record(0);
+  {
+    const auto ob = s.observables(member);  // initial state (set_state / discretize_initial)
+    rows.push_back({0, 0.0, ob.first, ob.second});
+  }
   const double norm0 = rows[0].norm;
+  const double invN = 1.0 / (double)s.N;
   for (std::int64_t k = 0; k < m;) {
     std::int64_t n = std::min(record_every, m - k);
-    step(n);
+    // observables fused into the passes: the exit
+    // pass that writes the samples also sums |u|^2 and v |u|^2 per member;
+    // the kinetic part comes out of the analysis exit pass of this member
+    s.enqueue_steps(n, nullptr, true);
+    const auto part = s.finish_obs(s.exit_blocks(false), s.batch)[(size_t)member];
+    s.coef.alloc(s.N);
+    s.analyze_dev(s.samples.p + member * s.N, s.coef.p, s.work.p, true);
+    const double kin = s.finish_obs(s.exit_blocks(true), 1)[0].second;
+    LD_CK(cudaGetLastError());
     k += n;
-    record(k);
+    rows.push_back({k, (double)k * s.dt_, std::sqrt(part.first * invN), kin + part.second * invN / s.eps});
     // norm-drift watchdog (numerical_invariant, CLI exit code 3)
     const double drift = std::fabs(rows.back().norm - norm0);
     if (p_->watchdog_tol > 0 && !(drift <= p_->watchdog_tol))

@@ -56,6 +56,7 @@ struct Nccl {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 
   static Nccl& get() {
     static Nccl n;
@@ -77,6 +78,7 @@ struct Nccl {
       sym(n.Recv, "ncclRecv");
       sym(n.AllReduce, "ncclAllReduce");
       sym(n.GetErrorString, "ncclGetErrorString");
+      sym(n.CommGetAsyncError, "ncclCommGetAsyncError");
     });
     if (!n.h || !n.CommInitRank || !n.Send || !n.Recv)
       raise(Errc::nccl_error, "libnccl.so.2 not found or incomplete (dlopen)");
@@ -360,6 +362,19 @@ struct DistSolver::Impl {
     Wb = M2 / G;
   }
 
+  // asynchronous NCCL failures (a peer died, a network error) surface here
+  // instead of as a hang in the next synchronisation: polled after every
+  // exchange enqueue and after each step() (SURVEY.md §5 failure detection)
+  void check_async() {
+    if (!comm) return;
+    Nccl& n = Nccl::get();
+    if (!n.CommGetAsyncError) return;
+    ncclResult_t st = ncclSuccess;
+    LD_NCCL(n.CommGetAsyncError(comm, &st));
+    if (st != ncclSuccess && st != ncclInProgress)
+      raise(Errc::nccl_error, std::string("NCCL asynchronous error: ") + n.GetErrorString(st));
+  }
+
   void exchange(bool col_to_row) {
     const long long blk = Hb * Wb;
     if (rank < 0) {  // virtual ranks: device copies
@@ -390,6 +405,7 @@ struct DistSolver::Impl {
       }
     }
     LD_NCCL(n.GroupEnd());
+    check_async();
     if (col_to_row)
       LD_CK(cudaMemcpyAsync(R.B.p + g * blk, R.A.p + g * blk, blk * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
     else
@@ -685,6 +701,7 @@ void DistSolver::step(std::int64_t nsteps) {
   LD_CK(cudaSetDevice(p_->device));
   p_->enqueue_steps(nsteps);
   LD_CK(cudaStreamSynchronize(p_->stream));
+  p_->check_async();
 }
 
 double DistSolver::time_steps(std::int64_t nsteps) {

@@ -94,7 +94,12 @@ extern "C" {
 
 const char* lattdse_last_error(void) { return g_msg.c_str(); }
 int lattdse_last_error_code(void) { return g_code; }
-const char* lattdse_version(void) { return "lattdse-b200 0.1.0 (sm_100a)"; }
+#ifndef LATTDSE_EXPERIMENTAL
+#define LATTDSE_EXPERIMENTAL 0
+#endif
+const char* lattdse_version(void) {
+  return LATTDSE_EXPERIMENTAL ? "lattdse-b200 0.2.0 (sm_100a, experimental variants)" : "lattdse-b200 0.2.0 (sm_100a)";
+}
 
 int lattdse_lattice_create(int dim, int rank, const int64_t* gen, const int64_t* moduli, lattdse_lattice** out) {
   return guard([&] {

@@ -1,6 +1,8 @@
-// Snapshot write/read (include/lattdse/snapshot.hpp). The data file is
-// written through a temporary name and renamed, so a crash mid-write never
-// leaves a truncated snapshot under the final name.
+// Snapshot write/read (include/lattdse/snapshot.hpp). Data file and sidecar
+// are both written under temporary names, then renamed data first, sidecar
+// last; the sidecar carries the data file's FNV-1a checksum, so a crash
+// between the two renames (new data, old sidecar) is detected on read
+// instead of resuming stale state under new metadata.
 #include "lattdse/snapshot.hpp"
 
 #include <cstdio>
@@ -27,6 +29,19 @@ bool little_endian() {
   unsigned char c;
   std::memcpy(&c, &one, 1);
   return c == 1;
+}
+
+// FNV-1a 64 over the data bytes, in 8-byte words (the sidecar's data_fnv1a)
+std::uint64_t data_checksum(const std::complex<double>* data, std::int64_t count) {
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(data);
+  const std::int64_t nbytes = count * static_cast<std::int64_t>(sizeof(std::complex<double>));
+  std::uint64_t h = 1469598103934665603ull;
+  for (std::int64_t i = 0; i < nbytes; i += 8) {
+    std::uint64_t w;
+    std::memcpy(&w, p + i, 8);
+    h = (h ^ w) * 1099511628211ull;
+  }
+  return h;
 }
 
 std::string read_text(const std::string& path) {
@@ -56,8 +71,9 @@ void snapshot_write(const std::string& path, const Lattice& lat, const std::comp
   side.obj["step"] = json::Value::integer(meta.step);
   side.obj["time"] = json::Value::number(meta.time);
   side.obj["dt"] = json::Value::number(meta.dt);
+  side.obj["data_fnv1a"] = json::Value::string(hex64(data_checksum(data, n * meta.members)));
 
-  const std::string tmp = path + ".tmp";
+  const std::string tmp = path + ".tmp", side_tmp = path + ".json.tmp";
   {
     std::ofstream f(tmp, std::ios::binary | std::ios::trunc);
     if (!f) raise(Errc::io_error, "cannot create snapshot " + tmp);
@@ -66,12 +82,15 @@ void snapshot_write(const std::string& path, const Lattice& lat, const std::comp
     if (!f) raise(Errc::io_error, "short write to snapshot " + tmp);
   }
   {
-    std::ofstream f(path + ".json", std::ios::trunc);
-    if (!f) raise(Errc::io_error, "cannot create snapshot sidecar " + path + ".json");
+    std::ofstream f(side_tmp, std::ios::trunc);
+    if (!f) raise(Errc::io_error, "cannot create snapshot sidecar " + side_tmp);
     f << side.dump() << "\n";
     if (!f) raise(Errc::io_error, "short write to snapshot sidecar");
   }
   if (std::rename(tmp.c_str(), path.c_str()) != 0) raise(Errc::io_error, "cannot rename " + tmp + " to " + path);
+  const std::string side_path = path + ".json";
+  if (std::rename(side_tmp.c_str(), side_path.c_str()) != 0)
+    raise(Errc::io_error, "cannot rename " + side_tmp + " to " + side_path);
 }
 
 SnapshotMeta snapshot_probe(const std::string& path, const Lattice& lat) {
@@ -110,6 +129,9 @@ SnapshotMeta snapshot_read(const std::string& path, const Lattice& lat, std::com
   f.read(reinterpret_cast<char*>(data), static_cast<std::streamsize>(sizeof(std::complex<double>) * count));
   if (f.gcount() != static_cast<std::streamsize>(sizeof(std::complex<double>) * count))
     raise(Errc::io_error, "snapshot " + path + " is truncated");
+  json::Value side = json::parse(read_text(path + ".json"));
+  if (side.has("data_fnv1a") && side.at("data_fnv1a").s != hex64(data_checksum(data, count)))
+    raise(Errc::io_error, "snapshot " + path + " does not match its sidecar (data_fnv1a): interrupted write?");
   return m;
 }
 

@@ -5,6 +5,10 @@ conservation to 1e-12 and time-reversibility to 1e-10).
 
 Both run the three-level layout (M = M1 x Ma x Mb), the device setup (norm
 table, sampling) and, at full N, the lean table schedule (peak ~148 GB)."""
+import hashlib
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -19,11 +23,28 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "c4r_tables.json")
+
+
+def c4r_norms(lat):
+    """The C4r norm table for the oracle: the device walk's table, admitted
+    only if it hashes to the ORACLE's own shell walk (tests/golden/
+    make_c4r_golden.py, committed sha256) -- so the oracle's input is the
+    oracle's index map, not the product's."""
+    norm2, mx = L.aaset_norms_device(lat)
+    gold = json.load(open(GOLD))
+    gen, moduli = lat.generators()
+    assert [int(x) for x in gen[0]] == gold["z"] and int(moduli[0]) == gold["n"]
+    assert hashlib.sha256(np.ascontiguousarray(norm2, np.uint32).tobytes()).hexdigest() == gold["norm2_sha256"]
+    assert int(mx) == gold["max_norm2"]
+    return norm2
+
+
 def test_config4_reduced_vs_oracle():
     cfg = configs.CONFIGS["C4r"]
     lat = configs.lattice(cfg)
     a, b, c, p = configs.problem(cfg)
-    norm2, mx = L.aaset_norms_device(lat)  # equal to the host walk (tests/test_gpu_setup.py)
+    norm2 = c4r_norms(lat)
     gen, moduli = lat.generators()
     orc = Oracle(gen, moduli, norm2, cfg.eps, a, b)
     orc.set_dt(cfg.dt)
@@ -71,7 +92,7 @@ def test_config4_reduced_sharded_virtual_ranks(world):
     cfg = configs.CONFIGS["C4r"]
     lat = configs.lattice(cfg)
     a, b, c, p = configs.problem(cfg)
-    norm2, _ = L.aaset_norms_device(lat)
+    norm2 = c4r_norms(lat)
     gen, moduli = lat.generators()
     orc = Oracle(gen, moduli, norm2, cfg.eps, a, b)
     orc.set_dt(cfg.dt)

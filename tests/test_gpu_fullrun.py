@@ -13,7 +13,7 @@ builds (device shell walk for rank 1, host walk for rank 2) must hash to the
 oracle's: the index map is compared bit-exactly.
 
 Config 3 runs the benched configuration itself: all 512 members in one
-group (the 1080 x 486 ensemble geometry bench.py times), members 0, 255, 511
+group (the 486 x 1080 ensemble geometry bench.py times), members 0, 255, 511
 checked.
 """
 import hashlib
@@ -77,7 +77,7 @@ def test_full_run_vs_oracle_fixture(name):
     members = [int(m) for m in fx["members"]]
     if name == "C3":
         info = S.info()
-        assert S.batch == 512 and info["group"] == 512 and (info["M1"], info["M2"]) == (1080, 486), info
+        assert S.batch == 512 and info["group"] == 512 and (info["M1"], info["M2"]) == (486, 1080), info
     S.step(1)
     for mi, mem in enumerate(members):
         got = S.get_state(L.COEFFICIENTS, m0=mem, count=1)[0]

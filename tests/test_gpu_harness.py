@@ -87,3 +87,98 @@ def test_second_order_convergence_config1():
     # needs dt << eps before the order shows)
     slope, errs = _slope(lat, 1.0, a, b, c, p, cfg.sigma, 0.1, (16, 32, 64, 128), 2048)
     assert 1.85 <= slope <= 2.15, (slope, errs)
+
+
+# ---------------------------------------------------------------------------
+# fused observables and the conservation study (§8(f) 4)
+def test_fused_observables_match_oracle():
+    """propagate's rows come from the fused exit-pass sums; they must equal
+    the CPU oracle's norm and energy at every record."""
+    from oracle.pyoracle import Oracle
+
+    cfg = configs.CONFIGS["C0"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    S = L.Solver(lat, cfg.eps, a, b, c, p, cfg.sigma, norm2=norm2)
+    S.set_dt(cfg.dt)
+    S.discretize_initial()
+    rows = S.propagate(64, 16)
+    gen, moduli = lat.generators()
+    orc = Oracle(gen, moduli, norm2, cfg.eps, a, b)
+    orc.set_dt(cfg.dt)
+    u = orc.analyze(orc.initial_samples(c[0], p[0], cfg.sigma))
+    for i, r in enumerate(rows):
+        if i:
+            u = orc.steps(u, 16)
+        assert int(r[0]) == 16 * i
+        assert abs(r[2] - orc.l2_norm(u)) <= 1e-12
+        e = orc.energy(u)
+        assert abs(r[3] - e) <= 1e-10 * abs(e), (i, r[3], e)
+
+
+def test_fused_observables_ensemble_member():
+    """The fused sums are per member: a propagate of member k reports that
+    member's norm and energy (checked against the unfused reductions)."""
+    cfg = configs.CONFIGS["C3"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg, batch=8)
+    S = _solver(lat, cfg.eps, a, b, c, p, cfg.sigma, cfg.dt)
+    rows = S.propagate(8, 4, member=5)
+    assert abs(rows[-1, 2] - S.l2_norm()[5]) <= 1e-13
+    assert abs(rows[-1, 3] - S.energy()[5]) <= 1e-11 * abs(rows[-1, 3])
+    with pytest.raises(L.LattdseError) as e:
+        S.propagate(4, 4, member=8)
+    assert e.value.name == "invalid_argument"
+
+
+def test_conservation_acceptance7_spec_scale(tmp_path):
+    """Acceptance 7 at its scale: d=5, eps=0.5, n=2^16,
+    dt=1/100, T=1 (the BASELINE seeded families stand in for g1/v2):
+    delta_norm <= 1e-10, delta_energy <= 1e-8 (delta = (max-min)/mean)."""
+    from paper_1808_06357_b200 import harness
+
+    z, _ = L.cbc_construct(1 << 16, 5)
+    lat = L.Lattice.rank1(z, 1 << 16)
+    a, b, c, p = L.problem_draw(7, 5, 1, 0.4, 0.6, 2)
+    S = _solver(lat, 0.5, a, b, c, p, 0.1, 0.01)
+    s = harness.run_conservation(S, 100, 1, config={"d": 5, "n": 1 << 16, "eps": 0.5}, out_dir=str(tmp_path))
+    assert s["records"] == 101
+    assert s["delta_norm"] <= 1e-10, s["delta_norm"]
+    assert s["delta_energy"] <= 1e-8, s["delta_energy"]
+    assert (tmp_path / "conservation.csv").exists() and (tmp_path / "conservation.json").exists()
+
+
+def test_conservation_config1_scale(tmp_path):
+    """The conservation study at config-1 scale (N = 1048583, d = 6,
+    eps = 0.05, 1024 steps, a record every 64 steps)."""
+    from paper_1808_06357_b200 import harness
+
+    cfg = configs.CONFIGS["C1"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    S = _solver(lat, cfg.eps, a, b, c, p, cfg.sigma, cfg.dt)
+    s = harness.run_conservation(S, cfg.m, 64, config={"config": "C1"}, out_dir=str(tmp_path))
+    assert s["records"] == cfg.m // 64 + 1
+    assert s["delta_norm"] <= 1e-10, s["delta_norm"]
+    assert s["delta_energy"] <= 1e-8, s["delta_energy"]
+
+
+def test_propagate_overhead_config1():
+    """Observables at record steps cost little over plain stepping: C1,
+    1024 steps, a record every 64 (fused sums + one analysis per record)."""
+    import time
+
+    cfg = configs.CONFIGS["C1"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    S = _solver(lat, cfg.eps, a, b, c, p, cfg.sigma, cfg.dt)
+    S.step(cfg.m)  # warm the graphs
+    S.propagate(64, 64)
+    t0 = time.perf_counter()
+    S.step(cfg.m)
+    t_step = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    S.propagate(cfg.m, 64)
+    t_prop = time.perf_counter() - t0
+    assert t_prop <= 1.10 * t_step, (t_prop, t_step)

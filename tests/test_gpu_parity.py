@@ -192,6 +192,8 @@ def test_config2_cluster_col_opt_in(cluster, monkeypatch):
     """Config 2 with the opt-in cluster COL pass (LATTDSE_CLUSTER_COL: each
     4096-long column split over a cluster of 8 or 4 CTAs through distributed
     shared memory, cluster_col.inl) against the oracle."""
+    if "experimental" not in L.version():
+        pytest.skip("cluster COL pass not in this build (make EXPERIMENTAL=1)")
     monkeypatch.setenv("LATTDSE_CLUSTER_COL", cluster)
     cfg = configs.CONFIGS["C2"]
     lat = configs.lattice(cfg)
@@ -279,6 +281,8 @@ def test_three_level_forced(geom, method, chunk, monkeypatch):
     chunk > 0 forces the L2-chunked row side (chunk rows of the M1 x M2 view
     at a time; 5 leaves a ragged last chunk), the opt-in LATTDSE_ROW_CHUNK."""
     if chunk:
+        if "experimental" not in L.version():
+            pytest.skip("L2 row chunks not in this build (make EXPERIMENTAL=1)")
         monkeypatch.setenv("LATTDSE_ROW_CHUNK", str(chunk))
     lat, a, b, c, p = configs.small_rank1(2, 4099, seed=31)
     eps, dt, sigma = 0.1, 1.0 / 64, 0.1

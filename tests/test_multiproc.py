@@ -73,7 +73,7 @@ def _worker(rank, world, port, batch, q):
     bufs = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(bufs, t)
     # bench's timing reduction: max over ranks
-    tmax = bench.max_over_ranks(float(rank + 1) * 1.5, dist, torch)
+    tmax = bench.reduce_over_ranks(float(rank + 1) * 1.5, dist, torch)
     if rank == 0:
         full = []
         for r in range(world):
@@ -101,3 +101,41 @@ def test_gloo_two_rank_ensemble_matches_single_process(batch):
     assert got.shape == want.shape
     assert np.array_equal(got, want)  # same arithmetic per member: bit-identical
     assert tmax == 3.0
+
+
+def test_bench_reference_arm_under_torchrun_two_ranks():
+    """bench.py --impl reference launched like the driver's N>1 arm
+    (torch.distributed.run, two ranks, gloo here): rank 0 alone runs and
+    prints ONE JSON line, the other rank exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--impl", "reference",
+           "--gpus", "2", "--config", "C0", "--steps", "2", "--warmup", "1", "--ref-seconds", "0.2"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["n_gpus"] == 2
+    assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_bench_respawns_ranks_without_launcher(monkeypatch):
+    """`bench.py --gpus N` with no WORLD_SIZE re-launches itself through
+    torch.distributed.run with N processes on 127.0.0.1."""
+    import sys
+
+    import bench
+
+    seen = {}
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2"])
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    bench.main()
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert "127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "4", "--steps", "2"]

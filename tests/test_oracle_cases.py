@@ -13,7 +13,7 @@ from oracle.cases import CASES, checksum_weights, checksums, subset_indices
 from oracle.scipy_port import ScipyPort
 
 
-@pytest.mark.parametrize("name", ["C0", "C1", "C2", "C3"])
+@pytest.mark.parametrize("name", ["C0", "C1", "C2", "C3", "C4r"])
 def test_cases_match_product_configs(name):
     cs, cfg = CASES[name], configs.CONFIGS[name]
     assert (cs.d, cs.N, cs.eps, cs.T, cs.m, cs.sigma, cs.batch) == (cfg.d, cfg.N, cfg.eps, cfg.T, cfg.m, cfg.sigma,
