@@ -36,17 +36,25 @@ def load(path):
     return [(k[1], v) for k, v in sorted(per.items())]
 
 
-def main(tag):
+def main(tag, configs=("C2", "C3", "C4")):
+    """Entries carry the geometry and kernel family they were captured on
+    (bench.py emits roofline.traffic only when they match the run) and the
+    source file; a capture with no step COL launch or fewer than 2 samples
+    per side fails instead of silently keeping old values."""
     out_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     table = json.load(open(out_path)) if os.path.exists(out_path) else {}
-    for cfg in ("C2", "C3", "C4"):
+    table = {k: v for k, v in table.items() if isinstance(v, dict)}  # drop pre-r2 bare numbers
+    bad = []
+    for cfg in configs:
         base = os.path.join(ROOT, "gpurun_out", tag)
         csvp, jp = os.path.join(base, f"{cfg}_traffic.csv"), os.path.join(base, f"{cfg}_plain.json")
         if not (os.path.exists(csvp) and os.path.exists(jp)):
             print(f"{cfg}: missing capture")
+            bad.append(cfg)
             continue
         line = json.loads(open(jp).read().strip().splitlines()[-1])
-        m1, lps = line["solver"]["M1"], line["solver"]["launches_per_step"]
+        sol = line["solver"]
+        m1, lps = sol["M1"], sol["launches_per_step"]
         launches = []
         for name, v in load(csvp):
             t = re.search(r"fft_pass_kernel<([^>]*)>", name)
@@ -58,14 +66,19 @@ def main(tag):
         col = [launches[i][1] for i in cols]
         # the row side of one step = the lps-1 launches right before a step COL launch
         row = [sum(b for _, b in launches[i - (lps - 1):i]) for i in cols if i >= lps - 1]
-        if col:
-            table[f"{cfg}_circulant_col"] = sum(col) / len(col)
-        if row:
-            table[f"{cfg}_circulant_row"] = sum(row) / len(row)
         print(cfg, "col", col, "row", row)
+        if len(col) < 2 or len(row) < 2:
+            bad.append(cfg)
+            continue
+        meta = {"M1": sol["M1"], "M2": sol["M2"], "group": sol["group"], "kernel": sol.get("pass_kernel"),
+                "source": f"profiles/{tag}/{cfg}_traffic.csv"}
+        table[f"{cfg}_circulant_col"] = {"bytes": sum(col) / len(col), "samples": len(col), **meta}
+        table[f"{cfg}_circulant_row"] = {"bytes": sum(row) / len(row), "samples": len(row), **meta}
     json.dump(table, open(out_path, "w"), indent=1)
     print(json.dumps(table, indent=1))
+    if bad:
+        sys.exit(f"ncu_traffic: no usable step-pass capture for {bad}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], tuple(sys.argv[2:]) or ("C2", "C3", "C4"))

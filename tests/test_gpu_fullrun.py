@@ -88,7 +88,9 @@ def test_full_run_vs_oracle_fixture(name):
         got = S.get_state(L.COEFFICIENTS, m0=mem, count=1)[0]
         check_state(got, fx, mi, "um", TOL_RUN)
         assert abs(norms[mem] - 1.0) <= TOL_NORM
-        assert abs(norms[mem] - float(fx[f"nrmm_{mi}"])) <= TOL_NORM
+        # the oracle's own norm drifts by up to ~2e-12 over C1's 4096
+        # recursive-FFT transforms (fixture nrmm 0.9999999999978751)
+        assert abs(norms[mem] - float(fx[f"nrmm_{mi}"])) <= 1e-11
         e_ref = float(fx[f"enm_{mi}"])
         assert abs(energies[mem] - e_ref) <= 1e-10 * abs(e_ref)
     if name == "C3":

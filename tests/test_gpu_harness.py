@@ -132,26 +132,62 @@ def test_fused_observables_ensemble_member():
     assert e.value.name == "invalid_argument"
 
 
+def _oracle_trajectory(z, n, eps, a, b, c, p, sigma, m, stride):
+    from oracle.pyoracle import Oracle, aaset
+
+    norm2, _ = aaset([list(map(int, z))], [n], with_vectors=False)
+    orc = Oracle([list(map(int, z))], [n], norm2, eps, a, b)
+    orc.set_dt(1.0 / m)
+    u = orc.analyze(orc.initial_samples(c, p, sigma))
+    nrm, en = [orc.l2_norm(u)], [orc.energy(u)]
+    for _ in range(m // stride):
+        u = orc.steps(u, stride)
+        nrm.append(orc.l2_norm(u))
+        en.append(orc.energy(u))
+    return np.array(nrm), np.array(en)
+
+
 def test_conservation_acceptance7_spec_scale(tmp_path):
-    """Acceptance 7 at its scale: d=5, eps=0.5, n=2^16,
-    dt=1/100, T=1 (the BASELINE seeded families stand in for g1/v2):
-    delta_norm <= 1e-10, delta_energy <= 1e-8 (delta = (max-min)/mean)."""
+    """The conservation study at acceptance 7's scale: d=5,
+    eps=0.5, n=2^16, dt=1/100, T=1, a record every step (the BASELINE
+    seeded families stand in for g1/v2).
+
+    delta_norm <= 1e-10 holds (unitary steps). SPEC's delta_energy <= 1e-8
+    does not hold for the Strang scheme at dt = 1/100: the energy of a
+    splitting method oscillates at O(dt^2) around a conserved modified
+    energy, and the CPU oracle shows the same 8.2e-4 (and 2.0e-4, 5.1e-5 at
+    dt = 1/200, 1/400). So the test pins the GPU trajectory to the
+    oracle's record by record (norm 1e-12, energy 1e-10 relative) and
+    checks the second-order scaling of delta_energy instead."""
     from paper_1808_06357_b200 import harness
 
-    z, _ = L.cbc_construct(1 << 16, 5)
-    lat = L.Lattice.rank1(z, 1 << 16)
+    n = 1 << 16
+    z, _ = L.cbc_construct(n, 5)
+    lat = L.Lattice.rank1(z, n)
     a, b, c, p = L.problem_draw(7, 5, 1, 0.4, 0.6, 2)
-    S = _solver(lat, 0.5, a, b, c, p, 0.1, 0.01)
-    s = harness.run_conservation(S, 100, 1, config={"d": 5, "n": 1 << 16, "eps": 0.5}, out_dir=str(tmp_path))
-    assert s["records"] == 101
-    assert s["delta_norm"] <= 1e-10, s["delta_norm"]
-    assert s["delta_energy"] <= 1e-8, s["delta_energy"]
-    assert (tmp_path / "conservation.csv").exists() and (tmp_path / "conservation.json").exists()
+    deltas = []
+    for m in (100, 200):
+        S = _solver(lat, 0.5, a, b, c, p, 0.1, 1.0 / m)
+        s = harness.run_conservation(S, m, m // 100, config={"d": 5, "n": n, "eps": 0.5, "m": m},
+                                     out_dir=str(tmp_path / f"m{m}"))
+        assert s["records"] == 101
+        assert s["delta_norm"] <= 1e-10, s["delta_norm"]
+        tr = np.loadtxt(tmp_path / f"m{m}" / "conservation.csv", delimiter=",", skiprows=1)
+        onrm, oen = _oracle_trajectory(z, n, 0.5, a, b, c[0], p[0], 0.1, m, m // 100)
+        assert np.max(np.abs(tr[:, 2] - onrm)) <= 1e-12
+        assert np.max(np.abs(tr[:, 3] - oen) / np.abs(oen)) <= 1e-10
+        assert abs(s["delta_energy"] - harness.variation(oen)) <= 1e-6 * harness.variation(oen)
+        deltas.append(s["delta_energy"])
+    assert 3.6 <= deltas[0] / deltas[1] <= 4.4, deltas  # O(dt^2)
 
 
 def test_conservation_config1_scale(tmp_path):
     """The conservation study at config-1 scale (N = 1048583, d = 6,
-    eps = 0.05, 1024 steps, a record every 64 steps)."""
+    eps = 0.05, 1024 steps, a record every 64 steps): norm conserved to
+    1e-10 (relative variation), the final energy equal to the oracle's
+    full-run fixture (tests/golden/run_C1.npz) to 1e-10 relative."""
+    import os
+
     from paper_1808_06357_b200 import harness
 
     cfg = configs.CONFIGS["C1"]
@@ -161,7 +197,11 @@ def test_conservation_config1_scale(tmp_path):
     s = harness.run_conservation(S, cfg.m, 64, config={"config": "C1"}, out_dir=str(tmp_path))
     assert s["records"] == cfg.m // 64 + 1
     assert s["delta_norm"] <= 1e-10, s["delta_norm"]
-    assert s["delta_energy"] <= 1e-8, s["delta_energy"]
+    tr = np.loadtxt(tmp_path / "conservation.csv", delimiter=",", skiprows=1)
+    fx = np.load(os.path.join(os.path.dirname(__file__), "golden", "run_C1.npz"))
+    e_ref = float(fx["enm_0"])
+    assert abs(tr[-1, 3] - e_ref) <= 1e-10 * abs(e_ref)
+    assert s["delta_energy"] <= 1e-5, s["delta_energy"]  # O(dt^2) oscillation, dt = 1/1024
 
 
 def test_propagate_overhead_config1():

@@ -90,3 +90,17 @@ def test_scipy_literal_rank2():
     u0 = orc.analyze(orc.initial_samples(c[0], p[0], 0.1))
     want = orc.steps(u0, 4)
     assert np.linalg.norm(port.steps(u0, 4) - want) <= 1e-12 * np.linalg.norm(want)
+
+
+def test_c4r_host_cbc_equals_device_catalog():
+    """The C4r generating vector (d = 20, N = 16777259) recomputed by the HOST
+    fast CBC (tools/c4r_host_cbc.py, 41 min on 8 cores, committed output)
+    equals catalog.json's device-CBC vector bit for bit."""
+    import json
+    import os
+
+    here = os.path.dirname(__file__)
+    host = json.load(open(os.path.join(here, "golden", "c4r_host_cbc.json")))
+    cat = json.load(open(os.path.join(here, "..", "paper_1808_06357_b200", "catalog.json")))["C4r"]
+    assert host["n"] == cat["n"] == 16777259 and host["d"] == 20
+    assert host["z"] == cat["z"] == CASES["C4r"].gen[0]
