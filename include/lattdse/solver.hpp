@@ -57,7 +57,7 @@ struct SolverInfo {
   int launches_per_step;
   std::int64_t group;
   std::int64_t row_chunk;  // three-level: M1 rows per L2-resident row-side chunk (0: whole view)
-  int pass3;               // 1: per-step passes on the persistent TMA-fed kernels (fft_pass3.cuh)
+  int pass4;               // 1: per-step passes have run on the lean plain-layout kernels (fft_pass4.cuh)
 };
 
 class Solver {

@@ -119,7 +119,7 @@ typedef struct lattdse_solver_info {
   int launches_per_step;
   int64_t M2a;       /* three-level inner split of M2 (0: two-level) */
   int64_t row_chunk; /* three-level: M1 rows per L2-resident row-side chunk (0: whole view) */
-  int pass3;         /* 1: the per-step passes run the persistent TMA-fed kernels (fft_pass3.cuh) */
+  int pass4;         /* 1: per-step passes have run on the lean plain-layout kernels (fft_pass4.cuh) */
 } lattdse_solver_info;
 
 /* Builds the anti-aliasing norm table, potential samples and device state. */

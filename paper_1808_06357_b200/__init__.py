@@ -263,7 +263,7 @@ class _Info(C.Structure):
                 ("M2", C.c_int64), ("group", C.c_int64), ("rank", C.c_int), ("method", C.c_int),
                 ("bytes_per_step", C.c_double), ("bytes_per_pass_col", C.c_double),
                 ("bytes_per_pass_row", C.c_double), ("launches_per_step", C.c_int), ("M2a", C.c_int64),
-                ("row_chunk", C.c_int64), ("pass3", C.c_int)]
+                ("row_chunk", C.c_int64), ("pass4", C.c_int)]
 
 
 METHODS = {"circulant": 0, "bluestein": 1}
@@ -387,7 +387,7 @@ class Solver:
         i = _Info()
         _ck(_lib.lattdse_solver_info_get(self._h, C.byref(i)))
         d = {k: getattr(i, k) for k, _ in _Info._fields_}
-        d["pass_kernel"] = "fft_pass3_kernel" if d["pass3"] else "fft_pass_kernel"
+        d["pass_kernel"] = "fft_pass4_kernel" if d["pass4"] else "fft_pass_kernel"
         return d
 
     def time_steps(self, nsteps: int) -> float:

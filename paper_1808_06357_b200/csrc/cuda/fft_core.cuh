@@ -266,13 +266,12 @@ constexpr int first_radix(int L) {
 
 // Explicit plans. The first four: long lines the greedy rule would end with
 // a radix-2/3 stage (three balanced stages instead). 1080: measured per
-// pass on config 3 (profiles/r2g, ms per launch over 512 members; the plan
-// is shared by both axes): as the ROW pass (9, 8, 15) 3.25 vs the greedy
-// (15, 12, 6) 4.10, (15, 8, 9) 3.57, (15, 9, 8) 4.09. Plans chosen by the
-// shared-memory wavefront model alone (tools/plan_search.py) lost where
-// they raised registers or put a large radix in the fused mid stage, which
-// holds the data and the prefetched diagonal together: ROW 486 (9, 6, 9)
-// 2.90 vs greedy (9, 9, 6) 2.74 ms despite 26% fewer wavefronts.
+// pass on config 3 with the lean pass4 kernels (profiles/r2/p4_sweep*.txt,
+// us per ROW launch over 64 members): (9, 12, 10) 283, (10, 12, 9) 287,
+// (9, 10, 12) 310, (15, 8, 9) 326, (9, 8, 15) 328 -- balanced task counts
+// per stage (120 / 90 / 108 tasks on 128 threads) and a small radix in the
+// fused mid stage, which holds the data and the prefetched diagonal
+// together, beat the larger radices. 486: (9, 9, 6) and (9, 6, 9) tie.
 struct PlanOverride {
   int L, r[4];
 };
@@ -290,7 +289,7 @@ constexpr PlanOverride kPlanOverride[] = {
     {kPlanX[0] ? kPlanX[0] : -1, {kPlanX[1], kPlanX[2], kPlanX[3], kPlanX[4]}},
     {kPlanY[0] ? kPlanY[0] : -1, {kPlanY[1], kPlanY[2], kPlanY[3], kPlanY[4]}},
     {2592, {9, 16, 18, 0}},  {3240, {15, 12, 18, 0}}, {3888, {27, 16, 9, 0}},
-    {4320, {15, 16, 18, 0}}, {1080, {9, 8, 15, 0}},   {0, {0, 0, 0, 0}},
+    {4320, {15, 16, 18, 0}}, {1080, {9, 12, 10, 0}},  {0, {0, 0, 0, 0}},
 };
 constexpr int override_radix(int L, int s) {
   for (const auto& o : kPlanOverride)

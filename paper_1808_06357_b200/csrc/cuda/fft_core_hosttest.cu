@@ -11,7 +11,7 @@
 #include <vector>
 #include <string>
 
-#include "fft_pass3.cuh"
+#include "fft_pass.cuh"
 
 using namespace lattdse_dev;
 using cld = std::complex<long double>;
@@ -101,89 +101,6 @@ void emulate(PassArgs a, int nlines, int nbatch) {
       Ctx<AXIS, L, B, PROG> c{sm.data(), a, blk * B, bat};
       run_pass<HostExec, AXIS, L, B, NT, PROG, SIGN1>(c);
     }
-}
-
-// pass3 path: the dense TMA tile (COL [row][B], ROW [B][L]; columns
-// beyond the view zero-filled like the TMA bounds check) + SRC_TMA stages
-// over the tile buffer and the extra ping-pong buffer (fft_pass3.cuh).
-template <int AXIS, int L, int B, int NT, int SIGN1>
-void emulate_v3(PassArgs a, int nlines, int nbatch) {
-  using G = Pass3Geom<AXIS, L, B>;
-  std::vector<double2> tile(G::buf_bytes / 16), wbuf(G::buf_bytes / 16);
-  const int nblk = (nlines + B - 1) / B;
-  for (int t = 0; t < nblk * nbatch; ++t) {
-    const int line0 = (t % nblk) * B;
-    const long long bat = t / nblk;
-    for (int b = 0; b < B; ++b)
-      for (int i = 0; i < L; ++i) {
-        const bool live = line0 + b < a.nlines;
-        const long long j = AXIS == AX_ROW ? (long long)(line0 + b) * L + i : (long long)i * a.ncols + (line0 + b);
-        tile[AXIS == AX_COL ? i * B + b : b * L + i] = live ? a.in[bat * a.in_bstride + j] : make_double2(0, 0);
-      }
-    Ctx<AXIS, L, B, PROG_DOUBLE> c{tile.data(), a, line0, bat, tile.data(), G::nbuf == 3 ? wbuf.data() : nullptr};
-    run_pass<HostExec, AXIS, L, B, NT, PROG_DOUBLE, SIGN1, SRC_TMA>(c);
-  }
-}
-
-// pass3 double program with a complex diag vs naive DFTs
-template <int AXIS, int L, int B, int NT, int SIGN1> void test_double_v3(int other, long long nmid, int pre, int post) {
-  int nrows = AXIS == AX_ROW ? other : L, ncols = AXIS == AX_ROW ? L : other;
-  std::mt19937_64 rng(L * 29 + AXIS + 3);
-  std::uniform_real_distribution<double> u(-1, 1);
-  long long n = (long long)nrows * ncols;
-  std::vector<double2> x(n), y(n), diag(n);
-  for (auto& v : x) v = make_double2(u(rng), u(rng));
-  for (auto& v : diag) v = make_double2(u(rng), u(rng));
-  y = x;
-  Tables tb;
-  tb.build(L, n);
-  tb.template build_plan<L>();
-  PassArgs a{};
-  a.in = y.data();
-  a.out = y.data();
-  a.in_bstride = a.out_bstride = n;
-  a.nvalid_in = a.nvalid_out = n;
-  a.nvalid_mid = nmid;
-  a.ncols = ncols;
-  a.nlines = AXIS == AX_ROW ? nrows : ncols;
-  a.diag_kind = DG_CPLX;
-  a.diag = diag.data();
-  a.pre_tw = pre;
-  a.post_tw = post;
-  a.fft_tw = tb.fft_tw.data();
-  a.fft_tw2 = tb.fft_tw2.data();
-  a.tw_lo = tb.tw_lo.data();
-  a.tw_hi = tb.tw_hi.data();
-  a.tw_shift = tb.shift;
-  emulate_v3<AXIS, L, B, NT, SIGN1>(a, AXIS == AX_ROW ? nrows : ncols, 1);
-  auto tw = [&](long long t) {
-    long double ang = -2.0L * kPi * (long double)(t % n) / (long double)n;
-    return cld(cosl(ang), sinl(ang));
-  };
-  double e = 0, mx = 0;
-  for (int line = 0; line < (AXIS == AX_ROW ? nrows : ncols); ++line) {
-    std::vector<cld> v(L);
-    auto idx = [&](int i) { return AXIS == AX_ROW ? (long long)line * L + i : (long long)i * ncols + line; };
-    for (int i = 0; i < L; ++i) {
-      v[i] = cld(x[idx(i)].x, x[idx(i)].y);
-      if (AXIS == AX_COL && pre) v[i] *= std::conj(tw((long long)line * i));
-    }
-    auto w = naive_dft(v, SIGN1);
-    for (int i = 0; i < L; ++i) {
-      long long j = idx(i);
-      w[i] = j < nmid ? w[i] * cld(diag[j].x, diag[j].y) : cld(0);
-    }
-    auto z = naive_dft(w, -SIGN1);
-    for (int i = 0; i < L; ++i) {
-      if (AXIS == AX_COL && post) z[i] *= tw((long long)line * i);
-      long long j = idx(i);
-      e = std::max(e, (double)std::abs(z[i] - cld(y[j].x, y[j].y)));
-      mx = std::max(mx, (double)std::abs(z[i]));
-    }
-  }
-  char buf[96];
-  std::snprintf(buf, sizeof buf, "pass3 double axis=%d L=%d B=%d NT=%d sign=%+d", AXIS, L, B, NT, SIGN1);
-  check(buf, e / mx, 4e-16 * 60);
 }
 
 // Lines along the contiguous (ROW) or strided (COL) axis: single transform.
@@ -456,19 +373,6 @@ int main(int argc, char** argv) {
     emulate<AX_COL, 1215, 2, 256, PROG_LOADDIAG, -1>(a, M2, 1);
     std::printf("c1 col entry emulated ok %f\n", buf[12345].x);
     return 0;
-  }
-  if (argc > 1 && std::string(argv[1]) == "v3") {
-    test_double_v3<AX_ROW, 1728, 1, 192, -1>(2, 3000, 0, 0);
-    test_double_v3<AX_COL, 1215, 2, 288, 1>(5, 2000, 1, 1);
-    test_double_v3<AX_ROW, 64, 4, 64, 1>(6, 300, 0, 0);
-    test_double_v3<AX_COL, 256, 4, 128, -1>(6, 900, 1, 1);
-    test_double_v3<AX_ROW, 4096, 1, 256, 1>(1, 3000, 0, 0);
-    test_double_v3<AX_COL, 720, 2, 160, 1>(3, 1500, 1, 0);
-    test_double_v3<AX_COL, 1080, 2, 384, 1>(7, 5000, 1, 1);
-    test_double_v3<AX_ROW, 486, 1, 96, -1>(3, 1000, 0, 0);
-    test_double_v3<AX_COL, 486, 4, 192, -1>(6, 2000, 1, 1);
-    std::printf(g_fail ? "SOME FAILED\n" : "ALL OK\n");
-    return g_fail;
   }
   if (argc > 1) {
     test_lines<AX_COL, 1215, 2, 256, -1>(4);

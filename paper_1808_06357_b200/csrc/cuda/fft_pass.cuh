@@ -13,14 +13,10 @@
 // Each stage is a radix-R Stockham step (in-register DFT_R, twiddles from a
 // correctly rounded table, one in-place shared-memory exchange).
 //
-// Two kernel shapes share the stage code:
-//  fft_pass_kernel  (v1): one CTA per tile of B lines; stage 0 loads straight
-//                   from global, the last stage stores straight to global.
-//  fft_pass3_kernel (fft_pass3.cuh, the per-step PROG_DOUBLE passes):
-//                   persistent CTAs; tile t+1 is brought into shared memory
-//                   by TMA (one elected thread, mbarrier completion) while
-//                   tile t is transformed; stage 0 reads the TMA tile
-//                   (SRC_TMA), the last stage stores straight to global.
+// fft_pass_kernel: one CTA per tile of B lines; stage 0 loads straight from
+// global, the last stage stores straight to global. It runs every program
+// and layout; the per-step PROG_DOUBLE passes of the plain layouts have a
+// leaner kernel of their own (fft_pass4.cuh).
 #pragma once
 
 #include "fft_core.cuh"
@@ -63,8 +59,6 @@ struct PassArgs {
   const double2* tw_hi;
   const double2* fft_tw;                   // per-stage twiddles, Plan<L>::tw_offset layout
   const double2* fft_tw2;                  // same for the reversed plan (second transform of PROG_DOUBLE)
-  int nblk;                                // pass3: line blocks per batch member
-  int ntiles;                              // pass3: nblk * batch
   // Good-Thomas (prime-factor) rank-1 layout: position (n1, n2) of the
   // M1 x M2 view holds natural index (M2*n1 + M1*n2) mod M, gcd(M1,M2)=1.
   int pfa;
@@ -98,6 +92,10 @@ struct PassArgs {
   const double* obs_w;
   const unsigned short* obs_widx;
   double obs_wscale;
+  // pass4 (fft_pass4.cuh): mid mask by rows for COL passes (nvalid_mid =
+  // mid_rb * ncols + mid_cb), and the L2 prefetch distance in tiles (0: off)
+  int mid_rb, mid_cb;
+  int pf;
 };
 
 // Shared-memory slots of one tile: B lines, each Plan<L>::phys-swizzled and
@@ -129,18 +127,13 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
   PassArgs a;  // by value: fields resolve to parameter-bank operands, not pointer loads
   int line0;
   long long bat;
-  // pass3: the TMA-filled tile (dense: COL i*B + b, ROW b*L + i) stage 0
-  // reads, and the odd ping-pong stage buffer (the tile's own buffer is
-  // the even one once stage 0 has consumed it)
-  const double2* tsrc = nullptr;
-  double2* sm1 = nullptr;
   mutable double acc0 = 0.0, acc1 = 0.0;  // fused observables (PassArgs::obs)
 
   static constexpr int LS = SmemGeom<L, B>::LS;
   LD_HD static int slot(int b, int i) { return b * LS + Plan<L>::phys(i); }
   // buffer used as the source of stage-sequence position p (0, 1, 2, ...)
   LD_HD double2* buf(int p) const {
-    return (SmemGeom<L, B>::pp && (p & 1)) ? (sm1 ? sm1 : sm + SmemGeom<L, B>::tile) : sm;
+    return (SmemGeom<L, B>::pp && (p & 1)) ? sm + SmemGeom<L, B>::tile : sm;
   }
 
   // array position of element (b, i) in the 2-D view
@@ -198,9 +191,6 @@ template <int AXIS, int L, int B, int PROG> struct Ctx {
     }
     return v;
   }
-  // pass3 stage-0 source: the TMA tile (PROG_DOUBLE passes, full input mask;
-  // columns beyond the view were zero-filled by the TMA bounds check)
-  LD_HD double2 tmaload(int b, int i) const { return tsrc[AXIS == AX_COL ? i * B + b : b * L + i]; }
   LD_HD void gstore(int b, int i, double2 v) const {
     if (!live(b)) return;
     long long j = out_index(b, i);
@@ -287,7 +277,7 @@ template <int R> struct Pow {
   }
 };
 
-enum : int { SRC_SMEM = 0, SRC_GLOBAL = 1, SRC_TMA = 2 };
+enum : int { SRC_SMEM = 0, SRC_GLOBAL = 1 };
 enum : int { DST_SMEM = 0, DST_SMEM_MID = 1, DST_GLOBAL = 2 };
 
 // Stage S of a transform, at position Q of the pass's stage sequence: reads
@@ -346,8 +336,6 @@ struct Stage {
           v[t][r] = c.buf(Q)[C::slot(b, j + r * T)];
         else if (SRC == SRC_GLOBAL)
           v[t][r] = c.gload(b, j + r * T);
-        else if (SRC == SRC_TMA)
-          v[t][r] = c.tmaload(b, j + r * T);
         else
           v[t][r] = c.buf(Q)[C::slot(b, j + r * T)];
       }

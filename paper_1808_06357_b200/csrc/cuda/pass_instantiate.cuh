@@ -2,11 +2,11 @@
 #pragma once
 
 #include "fft_pass.cuh"
-#include "fft_pass3.cuh"
+#include "fft_pass4.cuh"
 #include "pass_registry.hpp"
 
-#ifndef LATTDSE_BUILD_PASS3
-#define LATTDSE_BUILD_PASS3 1  // persistent TMA-fed per-step passes (fft_pass3.cuh)
+#ifndef LATTDSE_BUILD_PASS4
+#define LATTDSE_BUILD_PASS4 1  // lean per-step passes of the plain layouts (fft_pass4.cuh)
 #endif
 #ifndef LATTDSE_COL_B1_MIN
 #define LATTDSE_COL_B1_MIN 8192  // columns this long: one column per CTA
@@ -32,16 +32,55 @@ template <int AXIS, int L> struct Geometry {
                                                        : (L >= LATTDSE_COL_B1_MIN ? 1 : (L >= 512 && !col512 ? 2 : (L >= 128 ? 4 : 8)));
   static constexpr int raw = B * lattdse_dev::Plan<L>::max_tasks();
   static constexpr int NT = (wide_col || col512) ? 256 : (raw <= 32 ? 32 : (raw >= 512 ? 512 : ((raw + 31) / 32) * 32));
-  // pass3 (persistent, TMA-fed): CTAs per SM by shared memory, and the
-  // register cap that keeps that many resident
-  using G3 = lattdse_dev::Pass3Geom<AXIS, L, B>;
-  static constexpr int smem3 = G3::bytes;
-  static constexpr int ctas3 = (228 * 1024) / (smem3 + 1024);
-  // resident CTAs: as many as shared memory allows, at most what ~96
-  // registers per thread allow (the v1 kernels' budget; more registers cost
-  // warps, measured profiles/r2c: 166 regs -> 0.69x the warps on ROW 486)
-  static constexpr int by_regs = 65536 / (NT * 96) > 0 ? 65536 / (NT * 96) : 1;
-  static constexpr int mb3 = ctas3 < 1 ? 1 : (ctas3 < by_regs ? ctas3 : by_regs);
+};
+
+// pass4 launch geometry per (axis, L), from the sweeps of
+// fft_pass4_devtest (profiles/r2/p4_*.txt):
+//  ROW: one line per CTA (two below 512, more for short lines);
+//  COL: as many adjacent columns as an ~84 KB in-place tile holds, at most 8
+//       (128-byte row segments: 365 us vs 385 us for four columns at
+//       L = 486 over 64 members);
+//  NT covers the busiest stage; resident CTAs per SM as ~96 registers per
+//  thread and the shared memory allow (ROW 1080: 5 CTAs of 128 threads,
+//  283 us vs 326 us at 3 CTAs of 160).
+template <int AXIS, int L> struct Geometry4 {
+  using P = lattdse_dev::Plan<L>;
+  static constexpr bool ok = P::nst >= 2 && L >= 64;
+  static constexpr int B = AXIS == lattdse_dev::AX_ROW ? (L >= 512 ? 1 : (L >= 256 ? 2 : 256 / L * 2))
+                                                       : (L <= 648 ? 8 : (L <= 1296 ? 4 : (L <= 2592 ? 2 : 1)));
+  // threads: the multiple of 32 with the fewest thread slots over the stage
+  // sequence (a stage of t tasks runs ceil(t / NT) rounds of NT threads,
+  // each task R elements of work; the fused mid stage runs once with two
+  // transforms' worth, the others once per direction), at most two rounds
+  // per stage and those charged 25% extra (two tasks' registers live at
+  // once); ties to the larger CTA
+  static constexpr long long waste(int nt) {
+    long long w = 0;
+    for (int s = 0; s < P::nst; ++s) {
+      const int R = P::radix(s), t = B * (L / R), rounds = (t + nt - 1) / nt;
+      if (rounds > 2) return -1;
+      w += (long long)rounds * nt * R * (rounds > 1 ? 5 : 4);
+    }
+    return w;
+  }
+  static constexpr int pick_nt() {
+    int best = 512;
+    long long bw = -1;
+    for (int nt = 64; nt <= 512; nt += 32) {
+      const long long w = waste(nt);
+      if (w >= 0 && (bw < 0 || w <= bw)) {
+        bw = w;
+        best = nt;
+      }
+    }
+    return best;
+  }
+  static constexpr int NT = pick_nt();
+  static constexpr int smem = lattdse_dev::P4Geom<AXIS, L, B, 1>::bytes;
+  static constexpr int by96 = 65536 / (NT * 96), by72 = 65536 / (NT * 72);
+  static constexpr int by_regs = by96 >= 2 ? by96 : (by72 >= 2 ? 2 : 1);
+  static constexpr int by_smem = (227 * 1024) / (smem + 1024) > 0 ? (227 * 1024) / (smem + 1024) : 1;
+  static constexpr int MB = by_regs < by_smem ? by_regs : by_smem;
 };
 
 template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
@@ -65,10 +104,18 @@ template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
     // ROW lines of 4096 (radix-16 stages) spill heavily under the 3-CTA cap
     k.default_mb = G::wide_col ? 1 : (G::NT > 320 ? 2 : (AXIS == lattdse_dev::AX_ROW && L < 4096 ? 3 : 2));
   }
-  if constexpr (LATTDSE_BUILD_PASS3 && PROG == lattdse_dev::PROG_DOUBLE && G::smem3 <= 227 * 1024) {
-    k.fn3 = reinterpret_cast<const void*>(&lattdse_dev::fft_pass3_kernel<AXIS, L, G::B, G::NT, SIGN, G::mb3>);
-    k.smem3 = G::smem3;
-    k.boxr3 = G::G3::boxr;
+  if constexpr (LATTDSE_BUILD_PASS4 && PROG == lattdse_dev::PROG_DOUBLE && Geometry4<AXIS, L>::ok) {
+    using G4 = Geometry4<AXIS, L>;
+    using namespace lattdse_dev;
+    if constexpr (AXIS == AX_ROW) {
+      k.fn4[0] = reinterpret_cast<const void*>(&fft_pass4_kernel<AXIS, L, G4::B, 1, G4::NT, SIGN, false, DG_CPLX, G4::MB>);
+    } else {
+      k.fn4[0] = reinterpret_cast<const void*>(&fft_pass4_kernel<AXIS, L, G4::B, 1, G4::NT, SIGN, true, DG_CPLX, G4::MB>);
+      k.fn4[1] = reinterpret_cast<const void*>(&fft_pass4_kernel<AXIS, L, G4::B, 1, G4::NT, SIGN, false, DG_LUT16, G4::MB>);
+    }
+    k.B4 = G4::B;
+    k.NT4 = G4::NT;
+    k.smem4 = G4::smem;
   }
   register_pass_kernel(AXIS, L, PROG, SIGN, k);
 }

@@ -15,13 +15,13 @@ struct PassKernel {
   int NT = 0;                // threads per CTA
   int smem = 0;              // dynamic shared memory bytes
   bool attr_set = false;     // cudaFuncAttributeMaxDynamicSharedMemorySize applied
-  // pass3: persistent TMA-fed variant of the PROG_DOUBLE programs
-  // (fft_pass3.cuh); COL tiles arrive as boxr-row TMA boxes
-  const void* fn3 = nullptr;
-  int smem3 = 0;
-  int boxr3 = 0;
-  bool attr3_set = false;
-  int blocks_per_sm3 = 0;
+  // pass4: lean per-step variant of the PROG_DOUBLE programs on the plain
+  // layouts (fft_pass4.cuh). fn4[0]: complex diagonal (COL: with four-step
+  // twiddles; ROW: without); fn4[1]: COL, u16 norm index + LUT, no twiddles
+  // (the rank-2 grid's kinetic pass)
+  const void* fn4[2] = {};
+  int B4 = 0, NT4 = 0, smem4 = 0;
+  bool attr4_set = false;
   // PROG_DOUBLE instantiated with __launch_bounds__(NT, minBlocks) for
   // minBlocks = 1..4 (register cap vs occupancy); index 0 unused
   const void* fn_mb[5] = {};

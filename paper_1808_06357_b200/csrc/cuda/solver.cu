@@ -45,24 +45,6 @@ using namespace lattdse_dev;
 
 namespace lattdse {
 
-namespace {
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiledFn encode_tiled() {
-  static EncodeTiledFn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      p = nullptr;
-    return reinterpret_cast<EncodeTiledFn>(p);
-  }();
-  return fn;
-}
-}  // namespace
-
 #define LD_CK(x)                                                                                      \
   do {                                                                                                \
     cudaError_t e_ = (x);                                                                             \
@@ -532,12 +514,11 @@ struct Solver::Impl {
   bool bluestein_tables = false;
   long long launches = 0;
   bool sync_check = std::getenv("LATTDSE_SYNC_CHECK") != nullptr;  // debug: sync after every launch
-  // persistent TMA-fed per-step passes (fft_pass3.cuh), opt-in LATTDSE_PASS3=1
-  // until measured faster than the one-CTA-per-tile kernels (profiles/r2c)
-  bool use_pass3 = std::getenv("LATTDSE_PASS3") && std::atoi(std::getenv("LATTDSE_PASS3")) != 0;
-  int tma_promo = std::getenv("LATTDSE_TMA_PROMO") ? std::atoi(std::getenv("LATTDSE_TMA_PROMO")) : 0;
-  // COL tensor maps, one per (buffer, row length, rows, batch, batch stride)
-  std::map<std::tuple<const void*, int, int, long long, long long>, CUtensorMap> tmaps;
+  // lean per-step passes of the plain layouts (fft_pass4.cuh); LATTDSE_PASS4=0
+  // keeps every pass on the generic kernels (A/B runs, sanitizer coverage)
+  bool use_pass4 = !(std::getenv("LATTDSE_PASS4") && std::atoi(std::getenv("LATTDSE_PASS4")) == 0);
+  int pass4_pf = std::getenv("LATTDSE_PASS4_PF") ? std::atoi(std::getenv("LATTDSE_PASS4_PF")) : 0;  // L2 prefetch distance, tiles
+  long long launches4 = 0;
   int num_sms = 148;
   int minb_override = std::getenv("LATTDSE_MINB") ? std::atoi(std::getenv("LATTDSE_MINB")) : 0;
   // CUDA graphs of kGraphSteps identical middle steps, per (group start, size)
@@ -594,8 +575,10 @@ struct Solver::Impl {
     dev::PassKernel* k = dev::find_pass_kernel(axis, L, prog, sign);
     if (!k) raise(Errc::unsupported, "no pass kernel compiled for axis " + std::to_string(axis) + " L=" + std::to_string(L));
     a.nlines = (int)nlines;
-    if (use_pass3 && k->fn3 && prog == PROG_DOUBLE && pass3_ok(axis, L, a, nlines, k->B))
-      return launch_pass3(axis, L, k, a, nlines, nbatch);
+    if (use_pass4 && prog == PROG_DOUBLE && nbatch <= 65535) {
+      const int v4 = pass4_variant(axis, L, k, a, nlines);
+      if (v4 >= 0) return launch_pass4(axis, L, k, v4, a, nlines, nbatch);
+    }
     const void* fn = k->fn;
     if (prog == PROG_DOUBLE) {
       const int mb = minb_override > 0 ? minb_override : k->default_mb;
@@ -669,62 +652,44 @@ struct Solver::Impl {
                                       ": " + cudaGetErrorString(e));
     }
   }
-  // pass3 applies to the plain layouts with a full input mask (the TMA tile
-  // has no per-element mask); the sharded / Good-Thomas layouts keep v1
-  bool pass3_ok(int axis, int L, const PassArgs& a, long long nlines, int B) const {
-    if (a.pfa || a.rb_w > 0 || a.ncols_g > 0 || a.col_off != 0) return false;
-    if (axis == AX_COL) {
-      if (a.ncols < B || nlines != a.ncols || !encode_tiled()) return false;
-      if (a.nvalid_in < (long long)L * a.ncols || a.in_bstride < (long long)L * a.ncols) return false;
-    } else {
-      if (a.nvalid_in < nlines * (long long)L || (a.in_bstride < nlines * (long long)L && a.in_bstride != 0)) return false;
-    }
-    return (reinterpret_cast<uintptr_t>(a.in) & 15) == 0;
+  // pass4 serves the per-step double programs of the plain layouts: full
+  // tiles, no load / store masks, the twiddle and diagonal kinds its two
+  // instantiations cover (fft_pass4.cuh); everything else stays on v1.
+  // Returns the fn4 index or -1.
+  int pass4_variant(int axis, int L, const dev::PassKernel* k, const PassArgs& a, long long nlines) const {
+    if (!k->fn4[0] || a.pfa || a.rb_w > 0 || a.ncols_g > 0 || a.col_off != 0 || a.tw_mul > 1 || a.obs) return -1;
+    if (nlines % k->B4 != 0) return -1;
+    const long long span = axis == AX_COL ? (long long)L * a.ncols : nlines * (long long)L;
+    if (axis == AX_COL && nlines != a.ncols) return -1;
+    if (a.nvalid_in < span || a.nvalid_out < span) return -1;
+    if (a.in_bstride != 0 && a.in_bstride < span) return -1;
+    if (axis == AX_ROW) return (a.diag_kind == DG_CPLX && !a.pre_tw && !a.post_tw) ? 0 : -1;
+    if (a.diag_kind == DG_CPLX && a.pre_tw && a.post_tw) return 0;
+    if (a.diag_kind == DG_LUT16 && !a.pre_tw && !a.post_tw && k->fn4[1]) return 1;
+    return -1;
   }
-  const CUtensorMap& col_tmap(const PassArgs& a, int L, int boxr, int B, long long nbatch) {
-    auto key = std::make_tuple((const void*)a.in, a.ncols, L, nbatch, a.in_bstride);
-    auto it = tmaps.find(key);
-    if (it != tmaps.end()) return it->second;
-    CUtensorMap m;
-    std::memset(&m, 0, sizeof m);
-    const cuuint64_t dims[3] = {(cuuint64_t)2 * a.ncols, (cuuint64_t)L, (cuuint64_t)std::max<long long>(1, nbatch)};
-    const cuuint64_t strides[2] = {(cuuint64_t)a.ncols * 16, (cuuint64_t)std::max<long long>(1, a.in_bstride) * 16};
-    const cuuint32_t box[3] = {(cuuint32_t)(2 * B), (cuuint32_t)boxr, 1};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    const CUtensorMapL2promotion promo = tma_promo == 1   ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                                         : tma_promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                                         : tma_promo == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                                                          : CU_TENSOR_MAP_L2_PROMOTION_NONE;
-    const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(a.in), dims, strides,
-                                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
-                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) raise(Errc::device_error, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-    return tmaps.emplace(key, m).first->second;
-  }
-  void launch_pass3(int axis, int L, dev::PassKernel* k, PassArgs a, long long nlines, long long nbatch) {
-    if (!k->attr3_set) {
-      LD_CK(cudaFuncSetAttribute(k->fn3, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem3));
-      LD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k->blocks_per_sm3, k->fn3, k->NT, k->smem3));
-      k->attr3_set = true;
+  void launch_pass4(int axis, int L, dev::PassKernel* k, int v4, PassArgs a, long long nlines, long long nbatch) {
+    if (!k->attr4_set) {
+      for (const void* f : k->fn4)
+        if (f) LD_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem4));
+      k->attr4_set = true;
     }
     a.nlines = (int)nlines;
-    a.nblk = (int)((nlines + k->B - 1) / k->B);
-    const long long ntiles = (long long)a.nblk * nbatch;
-    if (ntiles > 0x7fffffffLL) raise(Errc::unsupported, "pass3: too many tiles");
-    a.ntiles = (int)ntiles;
-    CUtensorMap m;
-    std::memset(&m, 0, sizeof m);
-    if (axis == AX_COL) m = col_tmap(a, L, k->boxr3, k->B, nbatch);
-    const long long resident = (long long)std::max(1, k->blocks_per_sm3) * num_sms;
-    const dim3 grid((unsigned)std::min<long long>(ntiles, resident));
-    void* args[] = {&a, &m};
-    if (persist_bytes > 0 && a.diag_kind == DG_CPLX &&
-        ((axis == AX_ROW && (persist_mode & 1)) || (axis == AX_COL && (persist_mode & 2)))) {
+    const long long nmid = std::max<long long>(0, a.nvalid_mid);
+    a.mid_rb = (int)std::min<long long>(nmid / a.ncols, 0x7fffffff);
+    a.mid_cb = (int)(nmid % a.ncols);
+    a.pf = pass4_pf;
+    const dim3 grid((unsigned)(nlines / k->B4), (unsigned)nbatch);
+    void* args[] = {&a};
+    const void* fn = k->fn4[v4];
+    const bool persist_this = persist_bytes > 0 && a.diag_kind == DG_CPLX &&
+                              ((axis == AX_ROW && (persist_mode & 1)) || (axis == AX_COL && (persist_mode & 2)));
+    if (persist_this) {
       // keep the per-step diagonal table L2-resident (see launch_pass)
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = grid;
-      cfg.blockDim = dim3(k->NT);
-      cfg.dynamicSmemBytes = (size_t)k->smem3;
+      cfg.blockDim = dim3(k->NT4);
+      cfg.dynamicSmemBytes = (size_t)k->smem4;
       cfg.stream = stream;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
@@ -735,15 +700,16 @@ struct Solver::Impl {
       attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      LD_CK(cudaLaunchKernelExC(&cfg, k->fn3, args));
+      LD_CK(cudaLaunchKernelExC(&cfg, fn, args));
     } else {
-      LD_CK(cudaLaunchKernel(k->fn3, grid, dim3(k->NT), args, (size_t)k->smem3, stream));
+      LD_CK(cudaLaunchKernel(fn, grid, dim3(k->NT4), args, (size_t)k->smem4, stream));
     }
     ++launches;
+    ++launches4;
     if (sync_check) {
       cudaError_t e = cudaStreamSynchronize(stream);
       if (e != cudaSuccess)
-        raise(Errc::device_error, "pass3 axis=" + std::to_string(axis) + " L=" + std::to_string(L) + ": " +
+        raise(Errc::device_error, "pass4 axis=" + std::to_string(axis) + " L=" + std::to_string(L) + ": " +
                                       cudaGetErrorString(e));
     }
   }
@@ -1810,7 +1776,7 @@ SolverInfo Solver::info() const {
   i.rank = s.rank;
   i.method = s.method + (s.rank == 1 ? (s.pfa ? "/good-thomas" : "/four-step") : "");
   i.group = s.group;
-  i.pass3 = s.use_pass3 ? 1 : 0;  // used where a pass3 kernel is compiled and the layout is plain
+  i.pass4 = s.launches4 > 0 ? 1 : 0;  // the lean per-step kernels have run (plain layouts)
   // algorithmic bytes: every member's state read + written once per pass;
   // the diagonal tables are shared by the members of a group, so a launch
   // (one group) reads each table once

@@ -516,7 +516,7 @@ int lattdse_solver_info_get(lattdse_solver* s, lattdse_solver_info* out) {
     out->launches_per_step = i.launches_per_step;
     out->M2a = i.M2a;
     out->row_chunk = i.row_chunk;
-    out->pass3 = i.pass3;
+    out->pass4 = i.pass4;
   });
 }
 

@@ -4,12 +4,13 @@ have left a GPU unusable):
 
     compute-sanitizer --tool racecheck --error-exitcode 9 python tests/sanitize_case.py
 
-Covers the fused pass kernels' single-barrier ping-pong stages
-(fft_pass.cuh DevExec) on every program: C0 two-level circulant and the
+Covers the fused pass kernels' single-barrier ping-pong stages (the generic
+fft_pass.cuh kernels and the lean per-step fft_pass4.cuh kernels, which the
+solver picks for the plain layouts; LATTDSE_PASS4=0 runs the same cases on
+the generic kernels only) on every program: C0 two-level circulant and the
 literal Bluestein method, a three-level forced geometry, a rank-2 grid, an
-ensemble with a ragged last group, the fused observables (propagate), and
-the persistent TMA-fed pass3 kernels (LATTDSE_PASS3=1). Exits 0 with the
-solver results checked for finiteness and unit norm.
+ensemble with a ragged last group, and the fused observables (propagate).
+Exits 0 with the solver results checked for finiteness and unit norm.
 """
 import os
 import sys
@@ -50,8 +51,6 @@ def main():
     lat3 = configs.lattice(c3cfg)
     a4, b4, c4, p4 = configs.problem(c3cfg, batch=3)
     run(L.Solver(lat3, c3cfg.eps, a4, b4, c4, p4, c3cfg.sigma, group=2), 1)
-    if os.environ.get("LATTDSE_PASS3") == "1":
-        run(L.Solver(lat, cfg.eps, a, b, c, p, cfg.sigma), 2)
     print("sanitize_case: ok")
 
 

@@ -107,11 +107,10 @@ def test_shard_members_partition():
 
 
 def test_pass_kernel_emulation():
-    """nvcc-built host harness: every pass program (v1 and the pass3 TMA-tile path,
-    four-step and Good-Thomas layouts) vs naive long-double DFTs."""
+    """nvcc-built host harness: every pass program of the generic kernels
+    (four-step and Good-Thomas layouts) vs naive long-double DFTs."""
     exe = os.path.join(ROOT, "paper_1808_06357_b200", "csrc", "build", "fft_hosttest")
     subprocess.run(["make", "-C", os.path.join(ROOT, "paper_1808_06357_b200", "csrc"), "hosttest"], check=True,
                    stdout=subprocess.DEVNULL)
-    for arg in ([], ["v3"]):
-        out = subprocess.run([exe] + arg, capture_output=True, text=True, timeout=600)
-        assert out.returncode == 0 and "ALL OK" in out.stdout, out.stdout[-2000:]
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ALL OK" in out.stdout, out.stdout[-2000:]
