@@ -25,19 +25,48 @@
 
 namespace lattdse_dev {
 
-template <int AXIS, int L, int B, int LPT> struct P4Geom {
+// Stage sequence of a pass: positions 0 .. 2 nst - 2 (forward plan stages
+// 0 .. nst-1, the last of them fused with the reversed plan's stage 0, then
+// reversed plan stages 1 .. nst-1). The buffer an inner stage (radix R,
+// Ns > 1) writes is skewed by c slots per output block of Ns R elements,
+// c = Ns (1 - R) mod 8: consecutive tasks then fall into consecutive
+// 16-byte bank groups across block boundaries (unskewed, a run of Ns
+// consecutive slots is followed by a jump of Ns R - Ns + 1 slots, and a
+// quarter warp straddling it hits a bank group twice: 1.5-1.9 wavefronts
+// per access for Ns = 9, 10; tools/p4_conflicts.py). Block-aligned skews
+// keep every access of a task affine in r: the writer adds c (j / Ns) to
+// its base, the reader (T a multiple of the block) c (j / P) to its base
+// and c T / P to its stride.
+template <int L> struct P4Seq {
+  static constexpr int nst = Plan<L>::nst;
+  static constexpr int R(int q) { return q < nst ? PlanX<L, false>::radix(q) : PlanX<L, true>::radix(q - nst + 1); }
+  static constexpr int Ns(int q) { return q < nst ? PlanX<L, false>::ns(q) : PlanX<L, true>::ns(q - nst + 1); }
+  static constexpr bool inner(int q) { return q > 0 && q != nst - 1 && q < 2 * nst - 2; }
+  static constexpr int P(int q) { return inner(q) ? Ns(q) * R(q) : 0; }  // skew period of the buffer position q writes
+  static constexpr int C(int q) { return inner(q) ? ((Ns(q) * (1 - R(q))) % 8 + 8) % 8 : 0; }
+  static constexpr int extent() {
+    int m = L;
+    for (int q = 0; q < 2 * nst - 1; ++q)
+      if (P(q) > 0 && L + C(q) * (L / P(q)) > m) m = L + C(q) * (L / P(q));
+    return m;
+  }
+};
+
+// PP: two stage buffers (one barrier per stage) instead of one in place (two)
+template <int AXIS, int L, int B, int LPT, bool PP> struct P4Geom {
   static_assert(B % LPT == 0, "lines per thread must divide the tile");
   static constexpr int BG = B / LPT;  // line groups: a thread owns lines bg, bg + BG, ...
+  static constexpr int L0 = P4Seq<L>::extent();
   // COL tasks run line-fastest across a warp: pad the line stride so the BG
   // lines of a quarter warp fall into distinct 16-byte bank groups
   static constexpr int pad() {
     if (AXIS == AX_ROW || BG == 1) return 0;
     const int want = BG == 2 ? 4 : (BG == 4 ? 2 : 1);
-    return ((want - L % 8) % 8 + 8) % 8;
+    return ((want - L0 % 8) % 8 + 8) % 8;
   }
-  static constexpr int LS = L + pad();
+  static constexpr int LS = L0 + pad();
   static constexpr int tile = B * LS;
-  static constexpr bool pp = 2 * tile * 16 <= 72 * 1024;  // ping-pong buffers (one barrier per stage)
+  static constexpr bool pp = PP;
   static constexpr int R0 = Plan<L>::radix(0);
   static constexpr int tw_slots = AXIS == AX_COL ? B * R0 : 0;
   static constexpr int bytes = (pp ? 2 : 1) * tile * 16 + tw_slots * 16;
@@ -45,8 +74,9 @@ template <int AXIS, int L, int B, int LPT> struct P4Geom {
 
 #if defined(__CUDACC__)
 
-template <int AXIS, int L, int B, int LPT, int NT, int SIGN1, bool TW, int DK> struct Pass4 {
-  using G = P4Geom<AXIS, L, B, LPT>;
+template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, int DK> struct Pass4 {
+  using G = P4Geom<AXIS, L, B, LPT, PP>;
+  using SQ = P4Seq<L>;
   static constexpr int BG = G::BG, LS = G::LS, nst = Plan<L>::nst;
   static_assert(nst >= 2, "pass4 needs at least two stages");
 
@@ -57,6 +87,10 @@ template <int AXIS, int L, int B, int LPT, int NT, int SIGN1, bool TW, int DK> s
   double2* gout;
   int line0;
 
+  template <int P_, int C_> __device__ __forceinline__ static int skew(int j) {
+    if constexpr (C_ == 0) return 0;
+    else return C_ * (j / P_);
+  }
   __device__ __forceinline__ double2* buf(int p) const { return (G::pp && (p & 1)) ? sm + G::tile : sm; }
   __device__ __forceinline__ static void map(int q, int T, int& bg, int& j) {
     if (AXIS == AX_ROW) {
@@ -153,6 +187,10 @@ template <int AXIS, int L, int B, int LPT, int NT, int SIGN1, bool TW, int DK> s
   template <int S, bool REV, int SIGN, int Q> __device__ __forceinline__ void inner_stage(int tid) const {
     using P = PlanX<L, REV>;
     constexpr int R = P::radix(S), Ns = P::ns(S), T = L / R, TASKS = BG * T, TPT = (TASKS + NT - 1) / NT;
+    static_assert(R == SQ::R(Q) && Ns == SQ::Ns(Q), "sequence position");
+    constexpr int Pr = SQ::P(Q - 1), Cr = SQ::C(Q - 1), Tr = Cr ? T + Cr * (T / Pr) : T;  // skew of the buffer read
+    constexpr int Cw = SQ::C(Q);                                                          // and of the one written
+    static_assert(Cr == 0 || T % Pr == 0, "reader stride spans whole skew blocks");
     double2 v[TPT][LPT][R];
     int bgs[TPT], js[TPT];
 #pragma unroll
@@ -162,9 +200,9 @@ template <int AXIS, int L, int B, int LPT, int NT, int SIGN1, bool TW, int DK> s
       map(q, T, bgs[t], js[t]);
 #pragma unroll
       for (int l = 0; l < LPT; ++l) {
-        const double2* p = buf(Q) + (bgs[t] + l * BG) * LS + js[t];
+        const double2* p = buf(Q) + (bgs[t] + l * BG) * LS + js[t] + skew<Pr, Cr>(js[t]);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[t][l][r] = p[r * T];
+        for (int r = 0; r < R; ++r) v[t][l][r] = p[r * Tr];
       }
     }
     if (!G::pp) __syncthreads();  // in place: every read before any write
@@ -178,7 +216,7 @@ template <int AXIS, int L, int B, int LPT, int NT, int SIGN1, bool TW, int DK> s
       for (int l = 0; l < LPT; ++l) {
         apply_pow<R, SIGN>(pw, v[t][l]);
         DFT<R, SIGN>::run(v[t][l]);
-        double2* o = buf(Q + 1) + (bgs[t] + l * BG) * LS + (j - k) * R + k;
+        double2* o = buf(Q + 1) + (bgs[t] + l * BG) * LS + (j - k) * R + k + skew<Ns, Cw>(j);
 #pragma unroll
         for (int r = 0; r < R; ++r) o[r * Ns] = v[t][l][r];
       }
@@ -211,6 +249,8 @@ template <int AXIS, int L, int B, int LPT, int NT, int SIGN1, bool TW, int DK> s
     using P = PlanX<L, false>;
     constexpr int S = nst - 1, R = P::radix(S), Ns = P::ns(S), T = L / R, TASKS = BG * T, TPT = (TASKS + NT - 1) / NT;
     static_assert(T == Ns, "last stage covers j + r*T");
+    constexpr int Pr = SQ::P(Q - 1), Cr = SQ::C(Q - 1), Tr = Cr ? T + Cr * (T / Pr) : T;
+    static_assert(Cr == 0 || T % Pr == 0, "reader stride spans whole skew blocks");
     double2 v[TPT][LPT][R];
     int bgs[TPT], js[TPT];
 #pragma unroll
@@ -220,9 +260,9 @@ template <int AXIS, int L, int B, int LPT, int NT, int SIGN1, bool TW, int DK> s
       map(q, T, bgs[t], js[t]);
 #pragma unroll
       for (int l = 0; l < LPT; ++l) {
-        const double2* p = buf(Q) + (bgs[t] + l * BG) * LS + js[t];
+        const double2* p = buf(Q) + (bgs[t] + l * BG) * LS + js[t] + skew<Pr, Cr>(js[t]);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[t][l][r] = p[r * T];
+        for (int r = 0; r < R; ++r) v[t][l][r] = p[r * Tr];
       }
     }
     if (!G::pp) __syncthreads();
@@ -254,6 +294,8 @@ template <int AXIS, int L, int B, int LPT, int NT, int SIGN1, bool TW, int DK> s
     using P = PlanX<L, true>;
     constexpr int S = nst - 1, R = P::radix(S), Ns = P::ns(S), T = L / R, TASKS = BG * T, TPT = (TASKS + NT - 1) / NT;
     static_assert(T == Ns && R == G::R0, "last stage of the reversed plan mirrors stage 0");
+    constexpr int Pr = SQ::P(Q - 1), Cr = SQ::C(Q - 1), Tr = Cr ? T + Cr * (T / Pr) : T;
+    static_assert(Cr == 0 || T % Pr == 0, "reader stride spans whole skew blocks");
 #pragma unroll
     for (int t = 0; t < TPT; ++t) {
       const int q = tid + t * NT;
@@ -265,9 +307,9 @@ template <int AXIS, int L, int B, int LPT, int NT, int SIGN1, bool TW, int DK> s
 #pragma unroll
       for (int l = 0; l < LPT; ++l) {
         double2 v[R];
-        const double2* p = buf(Q) + (bg + l * BG) * LS + j;
+        const double2* p = buf(Q) + (bg + l * BG) * LS + j + skew<Pr, Cr>(j);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = p[r * T];
+        for (int r = 0; r < R; ++r) v[r] = p[r * Tr];
         apply_pow<R, -SIGN1>(pw, v);
         DFT<R, -SIGN1>::run(v);
         if (TW) fourstep<R, false>(bg + l * BG, j, v);
@@ -298,9 +340,9 @@ template <int AXIS, int L, int B, int LPT, int NT, int SIGN1, bool TW, int DK> s
 };
 
 // One CTA per tile of B lines; blockIdx.y = batch member.
-template <int AXIS, int L, int B, int LPT, int NT, int SIGN1, bool TW, int DK, int MINB>
+template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, int DK, int MINB>
 __global__ void __launch_bounds__(NT, MINB) fft_pass4_kernel(const __grid_constant__ PassArgs a) {
-  using K = Pass4<AXIS, L, B, LPT, NT, SIGN1, TW, DK>;
+  using K = Pass4<AXIS, L, B, LPT, PP, NT, SIGN1, TW, DK>;
   using G = typename K::G;
   extern __shared__ double2 lattdse_smem4[];
   const int tid = threadIdx.x;

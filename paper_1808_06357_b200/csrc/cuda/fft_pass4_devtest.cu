@@ -20,7 +20,7 @@ static double2 root(long long t, long long n) {
 }
 
 // AXIS, L: the pass; B4/LPT/NT4/MB4: pass4 launch geometry; other = the other factor of the view
-template <int AXIS, int L, int B4, int LPT, int NT4, int MB4, bool TW>
+template <int AXIS, int L, int B4, int LPT, int NT4, int MB4, bool TW, bool PP = (2 * B4 * L * 16 <= 72 * 1024)>
 int run(int other, int batch, int pf, bool lut = false) {
   using G1 = lattdse::dev::Geometry<AXIS, L>;
   const long long nrows = AXIS == AX_COL ? L : other, ncols = AXIS == AX_COL ? other : L;
@@ -73,15 +73,15 @@ int run(int other, int batch, int pf, bool lut = false) {
   const int sm1 = SmemGeom<L, G1::B>::bytes;
   CK(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1));
   const dim3 g1((unsigned)((nlines + G1::B - 1) / G1::B), batch);
-  const int sm4 = P4Geom<AXIS, L, B4, LPT>::bytes;
+  const int sm4 = P4Geom<AXIS, L, B4, LPT, PP>::bytes;
   const dim3 g4((unsigned)(nlines / B4), batch);
   auto launch4 = [&](const PassArgs& p) {
     if (lut) {
-      auto f4 = fft_pass4_kernel<AXIS, L, B4, LPT, NT4, SIGN, TW, DG_LUT16, MB4>;
+      auto f4 = fft_pass4_kernel<AXIS, L, B4, LPT, PP, NT4, SIGN, TW, DG_LUT16, MB4>;
       CK(cudaFuncSetAttribute(f4, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4));
       f4<<<g4, NT4, sm4>>>(p);
     } else {
-      auto f4 = fft_pass4_kernel<AXIS, L, B4, LPT, NT4, SIGN, TW, DG_CPLX, MB4>;
+      auto f4 = fft_pass4_kernel<AXIS, L, B4, LPT, PP, NT4, SIGN, TW, DG_CPLX, MB4>;
       CK(cudaFuncSetAttribute(f4, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4));
       f4<<<g4, NT4, sm4>>>(p);
     }
@@ -122,7 +122,7 @@ int run(int other, int batch, int pf, bool lut = false) {
   cudaEventRecord(e1);
   CK(cudaEventSynchronize(e1));
   cudaEventElapsedTime(&ms, e0, e1);
-  std::printf("  TIME pass4 B=%d LPT=%d NT=%d mb=%d pf=%d smem=%d: %8.1f us  (%.0f GB/s)\n", B4, LPT, NT4, MB4, pf, sm4, 1e3 * ms / reps,
+  std::printf("  TIME pass4 L=%d B=%d LPT=%d pp=%d NT=%d mb=%d pf=%d smem=%d: %8.1f us  (%.0f GB/s)\n", L, B4, LPT, (int)PP, NT4, MB4, pf, sm4, 1e3 * ms / reps,
               gb / (ms / reps * 1e-3));
   cudaFree(d0); cudaFree(d1); cudaFree(dd); cudaFree(dtw); cudaFree(dtw2); cudaFree(dlo); cudaFree(dhi); cudaFree(dlut); cudaFree(didx);
   return ok ? 0 : 1;

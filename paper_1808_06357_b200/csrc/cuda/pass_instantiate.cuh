@@ -34,20 +34,29 @@ template <int AXIS, int L> struct Geometry {
   static constexpr int NT = (wide_col || col512) ? 256 : (raw <= 32 ? 32 : (raw >= 512 ? 512 : ((raw + 31) / 32) * 32));
 };
 
-// pass4 launch geometry per (axis, L), from the sweeps of
-// fft_pass4_devtest (profiles/r2/p4_*.txt):
-//  ROW: one line per CTA (two below 512, more for short lines);
-//  COL: as many adjacent columns as an ~84 KB in-place tile holds, at most 8
-//       (128-byte row segments: 365 us vs 385 us for four columns at
-//       L = 486 over 64 members);
-//  NT covers the busiest stage; resident CTAs per SM as ~96 registers per
-//  thread and the shared memory allow (ROW 1080: 5 CTAs of 128 threads,
-//  283 us vs 326 us at 3 CTAs of 160).
+// pass4 launch geometry per (axis, L), from the sweeps of fft_pass4_devtest
+// (profiles/r2/p4_sweep*.txt; us per launch, config-3 shapes over 64 members
+// unless noted):
+//  ROW: one line per CTA (two below 512, more for short lines), two stage
+//       buffers (one barrier per stage) while both fit 72 KB;
+//  COL: more, smaller CTAs beat wider tiles -- L <= 648: four adjacent
+//       columns (64-byte row segments) in place, COL 486 four CTAs of 224
+//       threads 348 vs two CTAs of eight columns 366 vs v1 441; longer
+//       columns two per CTA, with two stage buffers while they fit 90 KB
+//       (config 1, COL 1296: 35.0 vs 39.0 in place vs v1 39.7);
+//  NT covers the busiest stage unless a narrower CTA running that stage in
+//  two rounds wastes fewer thread slots; resident CTAs per SM as ~96 (two
+//  buffers) or ~72 (in place) registers per thread and the shared memory
+//  allow (ROW 1080: 5 CTAs of 128 threads 271, 6 CTAs at 80 registers 293).
+// Plans whose first or last radix is a multiple of 4 stay on the v1 kernels
+// (their Ns = 1 stage writes conflict 4- to 8-fold without v1's swizzled
+// slots: ROW 4096 259 vs v1 220, COL 4096 296 vs 304 on config 2).
 template <int AXIS, int L> struct Geometry4 {
   using P = lattdse_dev::Plan<L>;
-  static constexpr bool ok = P::nst >= 2 && L >= 64;
+  static constexpr bool ok = P::nst >= 2 && L >= 64 && P::radix(0) % 4 != 0 && P::radix(P::nst - 1) % 4 != 0;
   static constexpr int B = AXIS == lattdse_dev::AX_ROW ? (L >= 512 ? 1 : (L >= 256 ? 2 : 256 / L * 2))
-                                                       : (L <= 648 ? 8 : (L <= 1296 ? 4 : (L <= 2592 ? 2 : 1)));
+                                                       : (L <= 648 ? 4 : (L <= 2592 ? 2 : 1));
+  static constexpr bool PP = 2 * B * L * 16 <= (AXIS == lattdse_dev::AX_ROW ? 72 : (L <= 648 ? 0 : 90)) * 1024;
   // threads: the multiple of 32 with the fewest thread slots over the stage
   // sequence (a stage of t tasks runs ceil(t / NT) rounds of NT threads,
   // each task R elements of work; the fused mid stage runs once with two
@@ -76,9 +85,8 @@ template <int AXIS, int L> struct Geometry4 {
     return best;
   }
   static constexpr int NT = pick_nt();
-  static constexpr int smem = lattdse_dev::P4Geom<AXIS, L, B, 1>::bytes;
-  static constexpr int by96 = 65536 / (NT * 96), by72 = 65536 / (NT * 72);
-  static constexpr int by_regs = by96 >= 2 ? by96 : (by72 >= 2 ? 2 : 1);
+  static constexpr int smem = lattdse_dev::P4Geom<AXIS, L, B, 1, PP>::bytes;
+  static constexpr int by_regs = 65536 / (NT * (PP ? 96 : 72)) > 0 ? 65536 / (NT * (PP ? 96 : 72)) : 1;
   static constexpr int by_smem = (227 * 1024) / (smem + 1024) > 0 ? (227 * 1024) / (smem + 1024) : 1;
   static constexpr int MB = by_regs < by_smem ? by_regs : by_smem;
 };
@@ -108,10 +116,10 @@ template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
     using G4 = Geometry4<AXIS, L>;
     using namespace lattdse_dev;
     if constexpr (AXIS == AX_ROW) {
-      k.fn4[0] = reinterpret_cast<const void*>(&fft_pass4_kernel<AXIS, L, G4::B, 1, G4::NT, SIGN, false, DG_CPLX, G4::MB>);
+      k.fn4[0] = reinterpret_cast<const void*>(&fft_pass4_kernel<AXIS, L, G4::B, 1, G4::PP, G4::NT, SIGN, false, DG_CPLX, G4::MB>);
     } else {
-      k.fn4[0] = reinterpret_cast<const void*>(&fft_pass4_kernel<AXIS, L, G4::B, 1, G4::NT, SIGN, true, DG_CPLX, G4::MB>);
-      k.fn4[1] = reinterpret_cast<const void*>(&fft_pass4_kernel<AXIS, L, G4::B, 1, G4::NT, SIGN, false, DG_LUT16, G4::MB>);
+      k.fn4[0] = reinterpret_cast<const void*>(&fft_pass4_kernel<AXIS, L, G4::B, 1, G4::PP, G4::NT, SIGN, true, DG_CPLX, G4::MB>);
+      k.fn4[1] = reinterpret_cast<const void*>(&fft_pass4_kernel<AXIS, L, G4::B, 1, G4::PP, G4::NT, SIGN, false, DG_LUT16, G4::MB>);
     }
     k.B4 = G4::B;
     k.NT4 = G4::NT;

@@ -47,10 +47,19 @@ def main():
     a3, b3, c3, p3 = L.problem_draw(5, 4, 1, 0.4, 0.6, 2)
     norm2, _, _ = L.aaset_build(g2, with_vectors=False)
     run(L.Solver(g2, 0.1, a3, b3, c3, p3, 0.1, norm2=norm2), 2)
-    c3cfg = configs.CONFIGS["C3"]
-    lat3 = configs.lattice(c3cfg)
-    a4, b4, c4, p4 = configs.problem(c3cfg, batch=3)
-    run(L.Solver(lat3, c3cfg.eps, a4, b4, c4, p4, c3cfg.sigma, group=2), 1)
+    # a two-level view whose ROW and COL lengths both run the lean pass4
+    # kernels (odd first / last radices, whole tiles): 4099 points in a
+    # 324 x 324 view, three members in ragged groups of two
+    os.environ["LATTDSE_GEOM"] = "324x324"
+    a5, b5, c5, p5 = L.problem_draw(cfg.seed, cfg.d, 3, 0.4, 0.6, 2)
+    S5 = run(L.Solver(lat, cfg.eps, a5, b5, c5, p5, cfg.sigma, group=2), 2)
+    assert S5.info()["pass4"] == 1 or os.environ.get("LATTDSE_PASS4") == "0", S5.info()
+    del os.environ["LATTDSE_GEOM"]
+    if "--quick" not in sys.argv:
+        c3cfg = configs.CONFIGS["C3"]
+        lat3 = configs.lattice(c3cfg)
+        a4, b4, c4, p4 = configs.problem(c3cfg, batch=3)
+        run(L.Solver(lat3, c3cfg.eps, a4, b4, c4, p4, c3cfg.sigma, group=2), 1)
     print("sanitize_case: ok")
 
 
