@@ -7,8 +7,10 @@ so this test only runs when LATTDSE_SANITIZE names ONE tool
     LATTDSE_SANITIZE=racecheck python -m pytest tests/test_gpu_sanitizer.py -m gpu -q
 
 (scripts/sanitize.sh runs it under gpurun, one call per tool) and is skipped
-in the plain `-m gpu` run. The logs of this round's runs are committed under
-profiles/r2/sanitizer_*.log; tests/test_profiles.py checks them.
+in the plain `-m gpu` run. Round 2: the pool's wrapper answers
+"compute-sanitizer is closed on this pool" (profiles/r2/sanitizer_closed.log),
+so the race evidence of this round is tests/test_gpu_pass4.py instead: the
+lean kernels against the generic ones, and bit-identical repeated runs.
 """
 import os
 import shutil
@@ -35,6 +37,8 @@ def test_compute_sanitizer_one_tool():
     os.makedirs(os.path.dirname(log), exist_ok=True)
     with open(log, "w") as f:
         f.write(out.stdout[-20000:] + "\n--- stderr ---\n" + out.stderr[-5000:] + f"\nrc={out.returncode}\n")
+    if "closed on this pool" in out.stderr or "closed on this pool" in out.stdout:
+        pytest.skip("compute-sanitizer is closed on this GPU pool (the box's wrapper refuses to run it)")
     assert out.returncode == 0, out.stdout[-3000:]
     assert "sanitize_case: ok" in out.stdout
     assert "ERROR SUMMARY: 0 errors" in out.stdout or "RACECHECK SUMMARY: 0 hazards" in out.stdout, out.stdout[-2000:]
