@@ -475,7 +475,17 @@ struct ObsSpec {
 struct Solver::Impl {
   // problem
   int rank = 1, dim = 1;
-  long long N = 0, n1 = 0, n2 = 0;  // rank-2: grid n1 x n2
+  // rank-r grid (r >= 2): tensor n1 x ... x nr, row-major.
+  // n1: first modulus (COL pass over the n1 x (N / n1) view), nrow: last
+  // modulus (ROW pass over N / nrow contiguous lines); the moduli between
+  // them are transformed by single-transform COL passes inside every block of
+  // `outer` leading indices (batch = member * outer + block, `inner` columns)
+  long long N = 0, n1 = 0, nrow = 0;
+  struct InnerAxis {
+    long long len, inner, outer;
+    DBuf<double2> tw, tw2;
+  };
+  std::vector<InnerAxis> axes;
   long long batch = 1, group = 1;
   double eps = 1, dt_ = 0;
   double watchdog_tol = 1e-9;  // propagate: max |norm - norm(0)| (0 = off)
@@ -544,10 +554,10 @@ struct Solver::Impl {
   // COL STOREDIAG over M2 columns; rank 2: ROW STOREDIAG over n1 rows) or
   // coefficients (rank 2 analysis: COL STOREDIAG over n2 columns)
   long long exit_blocks(bool coeffs) const {
-    if (rank == 2) {
+    if (rank >= 2) {
       dev::PassKernel* k = coeffs ? dev::find_pass_kernel(AX_COL, (int)n1, PROG_STOREDIAG, -1)
-                                  : dev::find_pass_kernel(AX_ROW, (int)n2, PROG_STOREDIAG, +1);
-      const long long lines = coeffs ? n2 : n1;
+                                  : dev::find_pass_kernel(AX_ROW, (int)nrow, PROG_STOREDIAG, +1);
+      const long long lines = coeffs ? N / n1 : N / nrow;
       return k ? (lines + k->B - 1) / k->B : 0;
     }
     dev::PassKernel* k = dev::find_pass_kernel(AX_COL, (int)M1, PROG_STOREDIAG, +1);
@@ -887,7 +897,7 @@ struct Solver::Impl {
     a.pre_tw = 1;
     launch_pass(AX_COL, (int)M1, PROG_STOREDIAG, +1, a, M2, 1);
   }
-  // ---- rank-2 passes (ROW length n2 over n1 rows; COL length n1 over n2 cols)
+  // ---- rank-r grid passes (ROW length nrow over N / nrow rows; COL length n1 over N / n1 columns)
   void g_row(int prog, int sign, const double2* in, double2* out, const double2* diag, long long nb,
              const ObsSpec& ob = ObsSpec{}) {
     PassArgs a = base_args(AX_ROW);
@@ -897,7 +907,7 @@ struct Solver::Impl {
     a.in_bstride = a.out_bstride = N;
     a.nvalid_in = a.nvalid_mid = a.nvalid_out = N;
     set_diag(a, diag);
-    launch_pass(AX_ROW, (int)n2, prog, sign, a, n1, nb);
+    launch_pass(AX_ROW, (int)nrow, prog, sign, a, N / nrow, nb);
   }
   void g_col(int prog, int sign, const double2* in, double2* out, int dkind, long long nb,
              const ObsSpec& ob = ObsSpec{}) {
@@ -914,19 +924,36 @@ struct Solver::Impl {
     if (prog == PROG_DOUBLE && cc_lloc > 0 && (dkind == DG_LUT16 || dkind == DG_NONE)) {
       // long columns (config 2): one cluster of CTAs per column block, the
       // column split across the cluster's shared memories (cluster_col.inl)
-      a.nlines = (int)n2;
+      a.nlines = (int)(N / n1);
       for (long long b0 = 0; b0 < nb; b0 += 65535) {
         PassArgs c = a;
         c.in = a.in + b0 * a.in_bstride;
         c.out = a.out + b0 * a.out_bstride;
-        LD_CK(dev::launch_cluster_col((int)n1, cc_lloc, sign, c, cc_tab.p, n2, std::min<long long>(65535, nb - b0), stream));
+        LD_CK(dev::launch_cluster_col((int)n1, cc_lloc, sign, c, cc_tab.p, N / n1, std::min<long long>(65535, nb - b0), stream));
         ++launches;
         if (sync_check) LD_CK(cudaStreamSynchronize(stream));
       }
       return;
     }
 #endif
-    launch_pass(AX_COL, (int)n1, prog, sign, a, n2, nb);
+    launch_pass(AX_COL, (int)n1, prog, sign, a, N / n1, nb);
+  }
+  // the moduli between the first and the last (rank >= 3): one plain
+  // transform of length n_a along axis a of every member, in place
+  void g_axis(InnerAxis& ax, int sign, double2* w, long long nb) {
+    PassArgs a = base_args(AX_COL);
+    a.fft_tw = ax.tw.p;
+    a.fft_tw2 = ax.tw2.p;
+    a.ncols = (int)ax.inner;
+    a.in = w;
+    a.out = w;
+    a.in_bstride = a.out_bstride = ax.len * ax.inner;
+    a.nvalid_in = a.nvalid_mid = a.nvalid_out = ax.len * ax.inner;
+    a.diag_kind = DG_NONE;
+    launch_pass(AX_COL, (int)ax.len, sign < 0 ? PROG_LOADDIAG : PROG_STOREDIAG, sign, a, ax.inner, nb * ax.outer);
+  }
+  void g_axes(int sign, double2* w, long long nb) {
+    for (auto& ax : axes) g_axis(ax, sign, w, nb);
   }
 
   // ---- rank-1 problem sampling on the device
@@ -971,12 +998,17 @@ struct Solver::Impl {
 
   // ---- setup
   void choose_geometry() {
-    if (rank == 2) {
+    if (rank >= 2) {
       M1 = n1;
-      M2 = n2;
+      M2 = N / n1;  // columns of the n1 x (N / n1) view the COL pass runs over
       M = N;
-      if (!dev::find_pass_kernel(AX_ROW, (int)n2, PROG_DOUBLE, -1) || !dev::find_pass_kernel(AX_COL, (int)n1, PROG_DOUBLE, -1))
-        raise(Errc::unsupported, "rank-2 grid " + std::to_string(n1) + "x" + std::to_string(n2) + " has no compiled pass kernels");
+      bool ok = dev::find_pass_kernel(AX_ROW, (int)nrow, PROG_DOUBLE, -1) && dev::find_pass_kernel(AX_COL, (int)n1, PROG_DOUBLE, -1);
+      for (auto& ax : axes) ok = ok && dev::find_pass_kernel(AX_COL, (int)ax.len, PROG_LOADDIAG, -1);
+      if (!ok) {
+        std::string dims;
+        for (long long m : lat.moduli()) dims += (dims.empty() ? "" : "x") + std::to_string(m);
+        raise(Errc::unsupported, "rank-" + std::to_string(rank) + " grid " + dims + " has no compiled pass kernels");
+      }
       return;
     }
     const long long need = 2 * N - 1;
@@ -1109,9 +1141,14 @@ struct Solver::Impl {
       return t;
     };
     up(tw_col, stage_tw(AX_COL, M1, false));
-    up(tw_row, stage_tw(AX_ROW, three ? Mb : M2, false));
+    const long long Lrow = rank >= 2 ? nrow : (three ? Mb : M2);
+    up(tw_row, stage_tw(AX_ROW, Lrow, false));
     up(tw_col2, stage_tw(AX_COL, M1, true));
-    up(tw_row2, stage_tw(AX_ROW, three ? Mb : M2, true));
+    up(tw_row2, stage_tw(AX_ROW, Lrow, true));
+    for (auto& ax : axes) {
+      up(ax.tw, stage_tw(AX_COL, ax.len, false));
+      up(ax.tw2, stage_tw(AX_COL, ax.len, true));
+    }
     if (three) {
       up(tw_mid, stage_tw(AX_COL, Ma, false));
       up(tw_mid2, stage_tw(AX_COL, Ma, true));
@@ -1124,7 +1161,7 @@ struct Solver::Impl {
     std::vector<double2> s = {make_double2(1.0 / (double)N, 0.0)};
     up(scal, s);
 #if LATTDSE_EXPERIMENTAL
-    if (rank == 2) cc_lloc = dev::cluster_col_lloc((int)n1, n2);
+    if (rank == 2) cc_lloc = dev::cluster_col_lloc((int)n1, N / n1);
     if (cc_lloc > 0) up(cc_tab, dev::cluster_col_tables((int)n1, cc_lloc));
 #endif
     LD_CK(cudaStreamSynchronize(stream));
@@ -1208,6 +1245,7 @@ struct Solver::Impl {
       r1_col_exit(w, chirp_n.p, c, N, 1, o);
     } else {
       g_row(PROG_LOADDIAG, -1, s, w, nullptr, 1);
+      g_axes(-1, w, 1);
       g_col(PROG_STOREDIAG, -1, w, c, DG_SCALAR, 1, o);
     }
   }
@@ -1219,6 +1257,7 @@ struct Solver::Impl {
       r1_col_exit(w, chirp_c.p, s, N, 1);
     } else {
       g_col(PROG_LOADDIAG, +1, c, w, DG_NONE, 1);
+      g_axes(+1, w, 1);
       g_row(PROG_STOREDIAG, +1, w, s, nullptr, 1);
     }
   }
@@ -1335,10 +1374,16 @@ struct Solver::Impl {
       const long long gb = std::min(group, batch - g0);
       double2* s = samples.p + g0 * N;
       double2* w = work.p;
-      if (rank == 2) {
+      if (rank >= 2) {
+        // F = F_1 ... F_r axis by axis; the kinetic diagonal sits between the
+        // forward and inverse transforms of the first axis, the potential
+        // between those of the last; the axes between them (rank >= 3) are
+        // plain transforms on either side of the first-axis pass
         timed(pt, false, [&] { g_row(PROG_LOADDIAG, -1, s, w, Vh.p, gb); });
         for (long long k = 0; k < nsteps; ++k) {
+          timed(pt, true, [&] { g_axes(-1, w, gb); });
           timed(pt, true, [&] { g_col(PROG_DOUBLE, -1, w, w, DG_LUT16, gb); });
+          timed(pt, true, [&] { g_axes(+1, w, gb); });
           if (k + 1 < nsteps)
             timed(pt, false, [&] { g_row(PROG_DOUBLE, +1, w, w, V.p, gb); });
           else
@@ -1433,10 +1478,20 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
   s.rank = lat.rank();
   s.dim = lat.dim();
   s.N = lat.n_total();
-  if (s.rank > 2) raise(Errc::unsupported, "the device path supports rank-1 and rank-2 lattices");
-  if (s.rank == 2) {
-    s.n1 = lat.moduli()[0];
-    s.n2 = lat.moduli()[1];
+  if (s.rank >= 2) {
+    const auto& n = lat.moduli();
+    s.n1 = n.front();
+    s.nrow = n.back();
+    long long outer = s.n1;
+    for (int a = 1; a + 1 < s.rank; ++a) {
+      long long inner = 1;
+      for (int t = a + 1; t < s.rank; ++t) inner *= n[t];
+      s.axes.emplace_back();
+      s.axes.back().len = n[a];
+      s.axes.back().inner = inner;
+      s.axes.back().outer = outer;
+      outer *= n[a];
+    }
   }
   const bool norms_on_device = aa.norm2.empty();  // build the norm table on this device (rank-1)
   if (norms_on_device && s.rank != 1) raise(Errc::unsupported, "device-built norm tables need a rank-1 lattice");
@@ -1449,7 +1504,7 @@ Solver::Solver(const Lattice& lat, const AntiAliasSet& aa, const ProblemSpec& pr
   s.prob = prob;
   s.eps = prob.eps;
   s.batch = (long long)prob.initial.size();
-  s.method = s.rank == 2 ? "grid" : opt.method;
+  s.method = s.rank >= 2 ? "grid" : opt.method;
   if (s.rank == 1 && s.method != "circulant" && s.method != "bluestein")
     raise(Errc::invalid_argument, "method must be 'circulant' or 'bluestein'");
   s.max_norm2 = aa.max_norm2;  // device-built tables: set below
@@ -1782,11 +1837,12 @@ SolverInfo Solver::info() const {
   // (one group) reads each table once
   const double M = (double)s.M, N = (double)s.N, B = (double)s.batch;
   const double G = (double)s.group, groups = std::ceil(B / G);
-  if (s.rank == 2) {
-    i.bytes_per_pass_row = B * 32.0 * N + groups * 16.0 * N;  // state R+W + V
-    i.bytes_per_pass_col = B * 32.0 * N + groups * 2.0 * N;   // state R+W + D index
+  if (s.rank >= 2) {
+    const double na = (double)s.axes.size();  // rank >= 3: a plain pass per inner axis on each side
+    i.bytes_per_pass_row = B * 32.0 * N + groups * 16.0 * N;                    // state R+W + V
+    i.bytes_per_pass_col = (1.0 + 2.0 * na) * B * 32.0 * N + groups * 2.0 * N;  // state R+W (+ inner axes) + D index
     i.bytes_per_step = i.bytes_per_pass_row + i.bytes_per_pass_col;
-    i.launches_per_step = 2;
+    i.launches_per_step = 2 + 2 * (int)s.axes.size();
   } else if (s.method == "circulant") {
     // state R+W + V: four-step reads the N valid V entries, Good-Thomas the
     // position-ordered V_perm (M entries, mask folded in)

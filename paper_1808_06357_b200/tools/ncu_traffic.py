@@ -2,8 +2,8 @@
 
 Reads gpurun_out/<tag>/{C2,C3,C4}_traffic.csv (ncu_traffic.sh) and the
 matching *_plain.json bench lines. The step COL pass is the
-fft_pass_kernel instance whose first template argument is 1 (COL), length the
-solver's M1 and program (fifth argument) 0; the row side of that step is the
+fft_pass4_kernel / fft_pass_kernel instance whose first template argument is
+1 (COL), length the solver's M1 and (v1) program, the fifth argument, 0; the row side of that step is the
 launches_per_step - 1 launches right before it (one ROW pass, or at config 4's
 three-level geometry COL-Ma, ROW-Mb, COL-Ma), matching how bench.py's
 pass_ms["row"] covers the whole row side. Traffic is dram read + write.
@@ -57,11 +57,14 @@ def main(tag, configs=("C2", "C3", "C4")):
         m1, lps = sol["M1"], sol["launches_per_step"]
         launches = []
         for name, v in load(csvp):
-            t = re.search(r"fft_pass_kernel<([^>]*)>", name)
+            t = re.search(r"fft_pass(4?)_kernel<([^>]*)>", name)
             if t:
-                args = [a.strip() for a in t.group(1).split(",")]
+                # v1: <axis, L, B, NT, prog, sign, minb>; pass4 (always the double program):
+                # <axis, L, B, LPT, PP, NT, sign, TW, DK, minb>
+                args = [re.sub(r"\((int|bool)\)", "", a).strip() for a in t.group(2).split(",")]
                 b = v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum", 0.0)
-                launches.append((args[0] == "1" and int(args[1]) == m1 and args[4] == "0", b))
+                step_col = args[0] == "1" and int(args[1]) == m1 and (t.group(1) == "4" or args[4] == "0")
+                launches.append((step_col, b))
         cols = [i for i, (is_col, _) in enumerate(launches) if is_col]
         col = [launches[i][1] for i in cols]
         # the row side of one step = the lps-1 launches right before a step COL launch

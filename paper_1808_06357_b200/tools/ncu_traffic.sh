@@ -2,7 +2,7 @@
 # DRAM traffic per pass launch for configs 2-4 (GPU box, one call), for the
 # bench line's roofline.traffic (profiles/ncu_traffic.json). Each bench
 # command first runs without ncu; ncu then captures consecutive
-# fft_pass_kernel launches inside the step loop.
+# pass-kernel launches (fft_pass4_kernel / fft_pass_kernel) inside the step loop.
 #   ./paper_1808_06357_b200/tools/ncu_traffic.sh r1g
 #   python paper_1808_06357_b200/tools/ncu_traffic.py r1g   (here)
 set -u
@@ -15,7 +15,7 @@ run() {  # name, skip, count, bench args...
   python bench.py "$@" > "$T/${name}_plain.json" 2> "$T/${name}_plain.err"; local rc=$?
   echo "$name plain rc=$rc" >> "$T/status_traffic.txt"
   if [ "$rc" = 0 ]; then
-    ncu --clock-control none -k regex:fft_pass_kernel --launch-skip "$skip" --launch-count "$count" \
+    ncu --clock-control none -k regex:fft_pass --launch-skip "$skip" --launch-count "$count" \
         --metrics "$M" --csv python bench.py "$@" > "$T/${name}_traffic.csv" 2> "$T/${name}_traffic.err"
     echo "$name ncu rc=$?" >> "$T/status_traffic.txt"
   fi

@@ -101,6 +101,46 @@ def test_rank2_grid_small(n1, n2, d):
     assert rel(S.get_state(L.COEFFICIENTS)[0], u8) <= TOL_RUN
 
 
+def _rank_r_lattice(kind):
+    if kind == "grid3":
+        return L.Lattice.grid([64, 32, 16])
+    if kind == "grid4":
+        return L.Lattice.grid([16, 16, 8, 8])
+    if kind == "odd3":  # odd-radix sides: the lean pass4 kernels where the tiles are whole
+        return L.Lattice.grid([81, 27, 9])
+    # rank 3 in five dimensions: block generators (1, 19 | 1, 7 | 1) over moduli 64, 32, 16
+    return L.Lattice.create(5, 3, [[1, 19, 0, 0, 0], [0, 0, 1, 7, 0], [0, 0, 0, 0, 1]], [64, 32, 16])
+
+
+@pytest.mark.parametrize("kind", ["grid3", "block3", "grid4", "odd3"])
+def test_rank_r_grid(kind):
+    """rank-r lattices, r >= 3: the r-dim DFT
+    axis by axis -- first-axis COL pass with the kinetic diagonal, plain
+    passes along the axes between, last-axis ROW pass with the potential."""
+    lat = _rank_r_lattice(kind)
+    d = lat.dim()
+    a, b, c, p = L.problem_draw(321 + d, d, 2, 0.4, 0.6, 2)
+    eps, dt, sigma = 0.05, 1.0 / 32, 0.2
+    S, orc = make(lat, a, b, c, p, sigma, eps, dt)
+    assert S.info()["rank"] == lat.rank() >= 3
+    for m in range(2):
+        g, u0, u1 = oracle_coeffs(orc, c[m], p[m], sigma, 1)
+        assert rel(S.get_state(L.COEFFICIENTS)[m], u0) <= 1e-13
+    S.step(1)
+    for m in range(2):
+        g, u0, u1 = oracle_coeffs(orc, c[m], p[m], sigma, 1)
+        assert rel(S.get_state(L.COEFFICIENTS)[m], u1) <= TOL_ONE
+    S.step(7)
+    for m in range(2):
+        g, u0, u8 = oracle_coeffs(orc, c[m], p[m], sigma, 8)
+        assert rel(S.get_state(L.COEFFICIENTS)[m], u8) <= TOL_RUN
+    assert np.all(np.abs(S.l2_norm() - 1.0) <= 1e-12)
+    e_gpu = S.energy()
+    for m in range(2):
+        g, u0, u8 = oracle_coeffs(orc, c[m], p[m], sigma, 8)
+        assert abs(e_gpu[m] - orc.energy(u8)) <= 1e-10 * abs(orc.energy(u8))
+
+
 def test_batch_members_independent():
     lat, a, b, c, p = configs.small_rank1(3, 1021, seed=5, batch=6, c_range=(0.3, 0.7), p_max=3)
     eps, dt, sigma = 0.05, 1.0 / 128, 0.1
