@@ -57,10 +57,14 @@ class DistSolver {
   int world() const;
   /// bytes each rank sends per exchange (two exchanges per step)
   double exchange_bytes_per_rank() const;
+  /// device bytes one rank held at the peak of the last set_dt (its slabs,
+  /// the transient table slabs and the norm index): scales as 1/G
+  double table_peak_bytes() const;
 
   static void nccl_unique_id(void* out128);
 
  private:
+  void set_dt_full_table(double dt);
   struct Impl;
   std::unique_ptr<Impl> p_;
 };

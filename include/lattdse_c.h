@@ -193,6 +193,8 @@ int lattdse_dist_l2_norm(lattdse_dist* d, double* out);
 int lattdse_dist_time_steps(lattdse_dist* d, int64_t nsteps, double* ms);
 /* M, M1, M2 of the sharded view; bytes each rank sends per exchange (2/step) */
 int lattdse_dist_info(lattdse_dist* d, int64_t* M, int64_t* M1, int64_t* M2, double* exchange_bytes);
+/* device bytes one rank held at the peak of the last set_dt (slabs + transient table slabs + norm index) */
+int lattdse_dist_table_peak_bytes(lattdse_dist* d, double* bytes);
 /* three-level row layout M2 = Ma x Mb of config-4-sized N (Ma = Mb = 0: two-level) */
 int lattdse_dist_three_level(lattdse_dist* d, int64_t* Ma, int64_t* Mb);
 

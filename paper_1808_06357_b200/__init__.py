@@ -481,8 +481,10 @@ class DistSolver:
         _ck(_lib.lattdse_dist_info(self._h, C.byref(M), C.byref(M1), C.byref(M2), C.byref(xb)))
         Ma, Mb = C.c_int64(), C.c_int64()
         _ck(_lib.lattdse_dist_three_level(self._h, C.byref(Ma), C.byref(Mb)))
+        pk = C.c_double()
+        _ck(_lib.lattdse_dist_table_peak_bytes(self._h, C.byref(pk)))
         return {"M": M.value, "M1": M1.value, "M2": M2.value, "Ma": Ma.value, "Mb": Mb.value,
-                "exchange_bytes_per_rank": xb.value}
+                "exchange_bytes_per_rank": xb.value, "table_peak_bytes": pk.value}
 
 
 def snapshot_write(lat: Lattice, path: str, data, *, space: int = SAMPLES, step: int = 0, time: float = 0.0,

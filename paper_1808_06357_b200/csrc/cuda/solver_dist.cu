@@ -23,12 +23,15 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <mutex>
 #include <numeric>
 
 #include "fft_pass.cuh"
 #include "sampling.cuh"
+#include "aaset_dev.hpp"
 #include "lattdse/dist.hpp"
 #include "pass_registry.hpp"
 
@@ -132,6 +135,85 @@ __global__ void k_slab_sample_g(const R1Points P, const double* __restrict__ c, 
 __global__ void k_scale_slab(double2* __restrict__ x, long long n, double s) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     x[i] = make_double2(x[i].x * s, x[i].y * s);
+}
+// ---- propagator tables built slab by slab (no unsharded table anywhere)
+// c_j = exp(-pi i j^2 / N) (conj: +), j^2 reduced mod 2N exactly (solver.cu k_chirp)
+__device__ __forceinline__ double2 chirp_at(long long j, long long N, bool conj) {
+  unsigned long long q = (unsigned long long)(((unsigned __int128)j * (unsigned __int128)j) % (unsigned __int128)(2 * N));
+  double sgn = 1.0;
+  if (q >= (unsigned long long)N) {
+    q -= (unsigned long long)N;
+    sgn = -1.0;
+  }
+  double s, co;
+  sincospi((double)q / (double)N, &s, &co);
+  return make_double2(sgn * co, conj ? sgn * s : -sgn * s);
+}
+// natural index of column-slab position q
+__device__ __forceinline__ long long slab_nat(long long q, long long M2, long long Wb, long long col_off) {
+  const long long j1 = q / Wb;
+  return j1 * M2 + col_off + (q - j1 * Wb);
+}
+// potential phase exp(i coef v(p_j)) on a column slab (zeros for j >= N): V, V^(1/2)
+__global__ void k_slab_vphase(const R1Points P, const double* __restrict__ a, const double* __restrict__ b, double coef,
+                              long long M1, long long M2, long long Wb, long long col_off, double2* __restrict__ out) {
+  const long long n = M1 * Wb;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+    const long long j = slab_nat(q, M2, Wb, col_off);
+    double2 v = make_double2(0.0, 0.0);
+    if (j < P.N) {
+      double sn, cs;
+      sincos(coef * sample_v_point(P, j, a, b), &sn, &cs);
+      v = make_double2(cs, sn);
+    }
+    out[q] = v;
+  }
+}
+// what: 0 even wrap of the chirp c into length M, scaled (Bluestein kernel of the synthesis);
+//       1 conj chirp (j < N); 2 kinetic phase D_j / N (norm index + LUT) times conj chirp (j < N)
+__global__ void k_slab_chirp(int what, long long N, long long M, long long M1, long long M2, long long Wb, long long col_off,
+                             double scale, const unsigned short* __restrict__ nidx, const double2* __restrict__ lut,
+                             double2* __restrict__ out) {
+  const long long n = M1 * Wb;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+    const long long t = slab_nat(q, M2, Wb, col_off);
+    double2 v = make_double2(0.0, 0.0);
+    if (what == 0) {
+      if (t < N)
+        v = chirp_at(t, N, false);
+      else if (t > M - N)
+        v = chirp_at(M - t, N, false);
+      v = make_double2(v.x * scale, v.y * scale);
+    } else if (t < N) {
+      v = chirp_at(t, N, true);
+      if (what == 2) v = c_mul(lut[nidx[t]], v);
+    }
+    out[q] = v;
+  }
+}
+// K^ from F = FFT_M(zero-padded k) on a block-major row slab, in place. The
+// circulant kernel is k wrapped periodically, wrap(k)[t] = k[t] (t < N) and
+// k[t - (M - N)] (t > M - N); the second part is k without k[0], shifted by
+// M - N, so FFT_M(wrap k)[m] = F[m] + w_m (F[m] - k[0]), w_m = exp(2 pi i m N / M):
+// a pointwise map of F, no data moves between ranks. Slab position (row r of
+// block q, column c) holds frequency m = k1 + M1 k2, k1 = row_off + r and k2 the
+// column q Wb + c (three-level rows: column ka Mb + kb holds k2 = ka + Ma kb).
+__global__ void k_khat_finish(double2* __restrict__ F, double2 k0, long long N, long long M, long long M1, long long Hb,
+                              long long Wb, int G, long long row_off, long long Ma, long long Mb, double scale) {
+  const long long n = (long long)G * Hb * Wb;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const long long q = p / (Hb * Wb), rem = p - q * Hb * Wb, r = rem / Wb, c = rem - r * Wb;
+    const long long col = q * Wb + c;
+    const long long k2 = Ma > 0 ? (col / Mb) + Ma * (col % Mb) : col;
+    const unsigned long long m = (unsigned long long)(row_off + r) + (unsigned long long)M1 * (unsigned long long)k2;
+    const unsigned long long e = (unsigned long long)(((unsigned __int128)m * (unsigned __int128)N) % (unsigned __int128)M);
+    double sn, cs;
+    sincospi(2.0 * (double)e / (double)M, &sn, &cs);
+    const double2 w = make_double2(cs, sn);
+    const double2 f = F[p];
+    const double2 d = c_mul(w, make_double2(f.x - k0.x, f.y - k0.y));
+    F[p] = make_double2((f.x + d.x) * scale, (f.y + d.y) * scale);
+  }
 }
 __global__ void k_sumsq(const double2* __restrict__ x, long long n, double* __restrict__ out) {
   __shared__ double red[32];
@@ -362,6 +444,34 @@ struct DistSolver::Impl {
     Wb = M2 / G;
   }
 
+  // ---- sharded table build (set_dt): plain forward FFT_M of column slabs
+  // column slab `src` of local rank i -> A_i (FFT_M1 down the columns, four-step twiddle)
+  void col_forward(int i, const double2* src) {
+    PassArgs a = col_args(local[i]);
+    a.in = src;
+    a.out = rk[i].A.p;
+    a.diag_kind = DG_NONE;
+    a.post_tw = 1;
+    launch(AX_COL, (int)M1, PROG_LOADDIAG, -1, a, Wb);
+  }
+  // row slab B_i -> `dst` (row slab layout, the order K^ is stored in): FFT_M2 along the rows
+  void row_forward(int i, double2* dst) {
+    if (three) {
+      PassArgs a = mid_args();
+      a.in = a.out = rk[i].B.p;
+      a.post_tw = 1;
+      launch(AX_COL, (int)Ma, PROG_LOADDIAG, -1, a, Mb, Hb);
+    }
+    PassArgs a = row_args();
+    a.in = rk[i].B.p;
+    a.out = dst;
+    a.diag_kind = DG_NONE;
+    if (three) a.rb_w = 0;
+    launch(AX_ROW, (int)(three ? Mb : M2), PROG_LOADDIAG, -1, a, three ? Hb * Ma : Hb);
+  }
+  // peak device bytes this process held in slab buffers during set_dt
+  // (tests: it scales as 1/G; no unsharded table is ever allocated)
+  size_t table_peak_bytes = 0;
   // asynchronous NCCL failures (a peer died, a network error) surface here
   // instead of as a hang in the next synchronisation: polled after every
   // exchange enqueue and after each step() (SURVEY.md §5 failure detection)
@@ -550,13 +660,162 @@ void DistSolver::nccl_unique_id(void* out128) {
   std::memcpy(out128, &id, sizeof id);
 }
 
-// The propagator tables (K^ in ROW-pass order, V, V^(1/2)) come from an
-// unsharded Solver forced to this geometry, built for the call and freed
-// before the work slabs are allocated: each process holds the table solver
-// and its state slabs, then its slabs. When the slab tables do not fit next
-// to the table solver (config 4 at small G), they are staged through host
-// memory.
+// The propagator tables (K^ in ROW-pass order, V, V^(1/2)), slab by slab:
+// nothing of size M or N complex is ever allocated, so a rank's peak memory
+// is its slabs (1/G of the problem) plus the 2 N-byte norm index.
+//   V, V^(1/2): the potential sampled at the slab's own points (sampling.cuh,
+//       the same point function as the unsharded solver: identical bits);
+//   K^ = FFT_M(wrap(k)) / M, k = F_N^-1(D / N):
+//     1. B2^ = FFT_M(even wrap of the chirp) / M with the solver's own
+//        distributed forward transform (COL pass, exchange, ROW pass);
+//     2. k by Bluestein: (D/N . conj chirp) -> FFT_M -> x B2^ -> IFFT_M ->
+//        x conj chirp, i.e. one Strang-shaped round trip (COL entry,
+//        exchange, ROW mid, exchange, COL exit) with these tables;
+//     3. F = FFT_M(zero-padded k), then K^ = (F + w (F - k[0])) / M pointwise
+//        (k_khat_finish): the periodic wrap is a shift by M - N, a phase in
+//        the spectrum, so no data crosses slabs; k[0] is one all-reduce.
+// LATTDSE_DIST_TABLES=full keeps the round-1 path (a transient unsharded
+// Solver whose tables are sliced) for A/B runs; dimensions beyond the device
+// sampler's limit use it too.
 void DistSolver::set_dt(double dt) {
+  Impl& s = *p_;
+  LD_CK(cudaSetDevice(s.device));
+  s.have_dt = false;
+  const char* mode = std::getenv("LATTDSE_DIST_TABLES");
+  if ((mode && std::string(mode) == "full") || s.lat.dim() > kMaxDimDev) {
+    set_dt_full_table(dt);
+    return;
+  }
+  for (auto& r : s.rk) {
+    r.A.release();
+    r.B.release();
+    r.V.release();
+    r.Vh.release();
+    r.K.release();
+  }
+  const long long slab = s.slab();
+  const int nl = (int)s.local.size();
+  const int g1 = s.grid1d(slab);
+  size_t free0 = 0, free1 = 0, total_b = 0;
+  LD_CK(cudaMemGetInfo(&free0, &total_b));
+  // norm index (2 N bytes, replicated) and the kinetic LUT exp(-i eps dt 2 pi^2 s) / N
+  DBuf<unsigned short> nidx;
+  nidx.alloc((size_t)s.N);
+  std::uint32_t max_norm2 = s.aa.max_norm2;
+  if (s.aa.norm2.empty()) {
+    max_norm2 = dev::aaset_norms_device(s.lat, nidx.p, s.stream);
+  } else {
+    std::vector<unsigned short> ni((size_t)s.N);
+    for (long long c = 0; c < s.N; ++c) ni[(size_t)c] = (unsigned short)s.aa.norm2[(size_t)c];
+    LD_CK(cudaMemcpy(nidx.p, ni.data(), ni.size() * sizeof(unsigned short), cudaMemcpyHostToDevice));
+  }
+  if (max_norm2 > 65534) raise(Errc::unsupported, "||h||^2 above 65535 does not fit the uint16 norm index");
+  std::vector<double2> lut(max_norm2 + 1);
+  for (std::uint32_t q = 0; q <= max_norm2; ++q) {
+    long double a = -(long double)s.prob.eps * (long double)dt * 2.0L * kPiL * kPiL * (long double)q;
+    long double r = fmodl(a, 2.0L * kPiL);
+    lut[q] = make_double2((double)(cosl(r) / (long double)s.N), (double)(sinl(r) / (long double)s.N));
+  }
+  DBuf<double2> dlut;
+  dlut.alloc(lut.size());
+  LD_CK(cudaMemcpy(dlut.p, lut.data(), lut.size() * sizeof(double2), cudaMemcpyHostToDevice));
+
+  std::vector<DBuf<double2>> T(nl), C(nl);  // B2^ (row slab) and a column-slab scratch per local rank
+  for (int i = 0; i < nl; ++i) {
+    s.rk[i].A.alloc((size_t)slab);
+    s.rk[i].B.alloc((size_t)slab);
+    s.rk[i].K.alloc((size_t)slab);
+    T[i].alloc((size_t)slab);
+    C[i].alloc((size_t)slab);
+  }
+  // per-rank peak of this build: everything allocated since entry (work slabs
+  // A, B, K^, B2^, scratch, norm index, LUT) plus the state slab held before
+  LD_CK(cudaMemGetInfo(&free1, &total_b));
+  s.table_peak_bytes = (free0 > free1 ? free0 - free1 : 0) / (size_t)nl + (size_t)slab * sizeof(double2);
+  const double invM = 1.0 / (double)s.M;
+  auto chirp = [&](int what, int i, double scale, double2* out) {
+    k_slab_chirp<<<g1, 256, 0, s.stream>>>(what, s.N, s.M, s.M1, s.M2, s.Wb, s.local[i] * s.Wb, scale, nidx.p, dlut.p, out);
+    LD_CK(cudaGetLastError());
+  };
+  // 1. B2^ = FFT_M(even wrap of c) / M
+  for (int i = 0; i < nl; ++i) {
+    chirp(0, i, invM, C[i].p);
+    s.col_forward(i, C[i].p);
+  }
+  s.exchange(true);
+  for (int i = 0; i < nl; ++i) s.row_forward(i, T[i].p);
+  // 2. k = conj c . IFFT_M(B2^ . FFT_M(D/N . conj c)): conj chirp parked in K_i (column-slab sized)
+  for (int i = 0; i < nl; ++i) {
+    chirp(2, i, 1.0, C[i].p);
+    chirp(1, i, 1.0, s.rk[i].K.p);
+    s.col_forward(i, C[i].p);
+  }
+  s.exchange(true);
+  for (int i = 0; i < nl; ++i) {
+    double2* keep = s.rk[i].K.p;
+    s.rk[i].K.p = T[i].p;  // row_mid multiplies by K_i: B2^ for this round trip
+    s.row_mid(i);
+    s.rk[i].K.p = keep;
+  }
+  s.exchange(false);
+  for (int i = 0; i < nl; ++i) {
+    PassArgs a = s.col_args(s.local[i]);
+    a.in = s.rk[i].A.p;
+    a.out = C[i].p;
+    a.diag = s.rk[i].K.p;
+    a.pre_tw = 1;
+    s.launch(AX_COL, (int)s.M1, PROG_STOREDIAG, +1, a, s.Wb);
+  }
+  // k[0]: first element of global column 0 (rank 0), summed over the ranks
+  double k0[2] = {0.0, 0.0};
+  for (int i = 0; i < nl; ++i)
+    if (s.local[i] == 0) {
+      LD_CK(cudaMemcpyAsync(k0, C[i].p, sizeof(double2), cudaMemcpyDeviceToHost, s.stream));
+      LD_CK(cudaStreamSynchronize(s.stream));
+    }
+  k0[0] = s.allreduce_sum(k0[0]);
+  k0[1] = s.allreduce_sum(k0[1]);
+  // 3. F = FFT_M(k zero-padded) into K_i, then the wrap as a spectral phase
+  for (int i = 0; i < nl; ++i) s.col_forward(i, C[i].p);
+  s.exchange(true);
+  for (int i = 0; i < nl; ++i) {
+    s.row_forward(i, s.rk[i].K.p);
+    k_khat_finish<<<g1, 256, 0, s.stream>>>(s.rk[i].K.p, make_double2(k0[0], k0[1]), s.N, s.M, s.M1, s.Hb, s.Wb, s.G,
+                                            s.local[i] * s.Hb, s.three ? s.Ma : 0, s.three ? s.Mb : 1, invM);
+    LD_CK(cudaGetLastError());
+  }
+  LD_CK(cudaStreamSynchronize(s.stream));
+  T.clear();
+  C.clear();
+  nidx.release();
+  // V, V^(1/2) at the slab's own points
+  R1Points P{};
+  P.N = s.N;
+  P.d = s.lat.dim();
+  const auto steps = s.lat.numerator_steps();
+  for (int j = 0; j < P.d; ++j) P.z[j] = steps[0][j];
+  DBuf<double> da, db;
+  da.alloc(std::max<size_t>(1, s.prob.potential.a.size()));
+  db.alloc(std::max<size_t>(1, s.prob.potential.b.size()));
+  LD_CK(cudaMemcpy(da.p, s.prob.potential.a.data(), s.prob.potential.a.size() * sizeof(double), cudaMemcpyHostToDevice));
+  if (!s.prob.potential.b.empty())
+    LD_CK(cudaMemcpy(db.p, s.prob.potential.b.data(), s.prob.potential.b.size() * sizeof(double), cudaMemcpyHostToDevice));
+  for (int i = 0; i < nl; ++i) {
+    auto& r = s.rk[i];
+    r.V.alloc((size_t)slab);
+    r.Vh.alloc((size_t)slab);
+    k_slab_vphase<<<g1, 256, 0, s.stream>>>(P, da.p, db.p, -dt / s.prob.eps, s.M1, s.M2, s.Wb, s.local[i] * s.Wb, r.V.p);
+    k_slab_vphase<<<g1, 256, 0, s.stream>>>(P, da.p, db.p, -dt / (2.0 * s.prob.eps), s.M1, s.M2, s.Wb, s.local[i] * s.Wb, r.Vh.p);
+    LD_CK(cudaGetLastError());
+  }
+  LD_CK(cudaStreamSynchronize(s.stream));
+  s.have_dt = true;
+}
+
+// Round-1 path: a transient unsharded Solver, forced to the same geometry,
+// builds the tables; they are sliced into the slabs (staged through host
+// memory when they do not fit next to it).
+void DistSolver::set_dt_full_table(double dt) {
   Impl& s = *p_;
   LD_CK(cudaSetDevice(s.device));
   s.have_dt = false;
@@ -570,6 +829,8 @@ void DistSolver::set_dt(double dt) {
   const long long slab = s.slab();
   const size_t sb = (size_t)slab * sizeof(double2);
   std::vector<std::vector<double2>> host;  // staged [rank][table] when the slabs do not fit
+  size_t free_entry = 0, total_entry = 0;
+  LD_CK(cudaMemGetInfo(&free_entry, &total_entry));
   {
     SolverOptions so;
     so.device = s.device;
@@ -579,6 +840,11 @@ void DistSolver::set_dt(double dt) {
     so.group = 1;
     Solver full(s.lat, s.aa, s.prob, so);
     full.set_dt(dt);
+    {
+      size_t f1 = 0, tb = 0;
+      LD_CK(cudaMemGetInfo(&f1, &tb));
+      s.table_peak_bytes = (free_entry > f1 ? free_entry - f1 : 0) + (size_t)s.slab() * sizeof(double2);
+    }
     const auto* K = (const double2*)full.device_table(0);
     const auto* V = (const double2*)full.device_table(1);
     const auto* Vh = (const double2*)full.device_table(2);
@@ -734,6 +1000,7 @@ std::int64_t DistSolver::M1() const { return p_->M1; }
 std::int64_t DistSolver::M2() const { return p_->M2; }
 std::int64_t DistSolver::Ma() const { return p_->three ? p_->Ma : 0; }
 int DistSolver::world() const { return p_->G; }
+double DistSolver::table_peak_bytes() const { return (double)p_->table_peak_bytes; }
 double DistSolver::exchange_bytes_per_rank() const {
   return 16.0 * (double)p_->Hb * (double)p_->Wb * (double)(p_->G - 1);
 }

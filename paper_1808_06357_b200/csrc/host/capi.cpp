@@ -650,6 +650,14 @@ int lattdse_dist_info(lattdse_dist* d, int64_t* M, int64_t* M1, int64_t* M2, dou
   });
 }
 
+int lattdse_dist_table_peak_bytes(lattdse_dist* d, double* bytes) {
+  return guard([&] {
+    LD_NEED_D();
+    need(bytes, "bytes");
+    *bytes = d->d->table_peak_bytes();
+  });
+}
+
 int lattdse_dist_three_level(lattdse_dist* d, int64_t* Ma, int64_t* Mb) {
   return guard([&] {
     LD_NEED_D();
