@@ -282,6 +282,13 @@ struct DistSolver::Impl {
   int tw_shift = 0;
   ncclComm_t comm = nullptr;
   bool have_dt = false;
+  // row side in `chunks` row chunks (Hb % chunks == 0): the exchanges run on
+  // their own stream, chunk by chunk, under the row passes of the other
+  // chunks; 1: one blocking exchange each way
+  int chunks = 1;
+  cudaStream_t xstream = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_done;
+  cudaEvent_t ev_col = nullptr, ev_back = nullptr;
 
   explicit Impl(const Lattice& l) : lat(l) {}
 
@@ -569,15 +576,123 @@ struct DistSolver::Impl {
     }
   }
 
+  // rows [k Hc, (k+1) Hc) of every block, one way; on stream `st`
+  void exchange_chunk(bool col_to_row, int k, cudaStream_t st) {
+    const long long blk = Hb * Wb, Hc = Hb / chunks, off = (long long)k * Hc * Wb, cnt = Hc * Wb;
+    if (rank < 0) {
+      for (int g = 0; g < G; ++g)
+        for (int h = 0; h < G; ++h) {
+          if (col_to_row)
+            LD_CK(cudaMemcpyAsync(rk[h].B.p + g * blk + off, rk[g].A.p + h * blk + off, cnt * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, st));
+          else
+            LD_CK(cudaMemcpyAsync(rk[g].A.p + h * blk + off, rk[h].B.p + g * blk + off, cnt * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, st));
+        }
+      return;
+    }
+    Nccl& n = Nccl::get();
+    const int g = rank;
+    Rank& R = rk[0];
+    double2* src = col_to_row ? R.A.p : R.B.p;
+    double2* dst = col_to_row ? R.B.p : R.A.p;
+    LD_NCCL(n.GroupStart());
+    for (int h = 0; h < G; ++h) {
+      if (h == g) continue;
+      LD_NCCL(n.Send(src + h * blk + off, 2 * cnt, ncclDouble, h, comm, st));
+      LD_NCCL(n.Recv(dst + h * blk + off, 2 * cnt, ncclDouble, h, comm, st));
+    }
+    LD_NCCL(n.GroupEnd());
+    check_async();
+    LD_CK(cudaMemcpyAsync(dst + g * blk + off, src + g * blk + off, cnt * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  }
+  // the row side on rows [k Hc, (k+1) Hc) of local rank i's slab
+  void row_mid_chunk(int i, int k) {
+    const long long Hc = Hb / chunks, off = (long long)k * Hc * Wb;
+    double2* B = rk[i].B.p + off;
+    if (three) {
+      PassArgs a = mid_args();
+      a.in = a.out = B;
+      a.post_tw = 1;
+      launch(AX_COL, (int)Ma, PROG_LOADDIAG, -1, a, Mb, Hc);
+      // Mb-lines are contiguous inside a block only: one ROW launch per block
+      for (int q = 0; q < G; ++q) {
+        PassArgs r = row_args();
+        r.rb_w = 0;
+        r.in = r.out = B + (long long)q * Hb * Wb;
+        r.diag = rk[i].K.p + off + (long long)q * Hb * Wb;
+        r.in_bstride = r.out_bstride = Hc * Wb;
+        r.nvalid_in = r.nvalid_mid = r.nvalid_out = Hc * Wb;
+        launch(AX_ROW, (int)Mb, PROG_DOUBLE, -1, r, Hc * Wb / Mb);
+      }
+      PassArgs b = mid_args();
+      b.in = b.out = B;
+      b.pre_tw = 1;
+      launch(AX_COL, (int)Ma, PROG_STOREDIAG, +1, b, Mb, Hc);
+    } else {
+      PassArgs a = row_args();
+      a.in = a.out = B;
+      a.diag = rk[i].K.p + off;
+      launch(AX_ROW, (int)M2, PROG_DOUBLE, -1, a, Hc);
+    }
+  }
+  // exchange -> row passes -> exchange as a pipeline over row chunks: the
+  // copies of chunk k+2 (in) and chunk k (out) run on `xstream` under the
+  // row passes of chunk k+1 on `stream`
+  void row_side_pipelined() {
+    const int nl = (int)local.size();
+    LD_CK(cudaEventRecord(ev_col, stream));
+    LD_CK(cudaStreamWaitEvent(xstream, ev_col, 0));
+    auto in = [&](int k) {
+      exchange_chunk(true, k, xstream);
+      LD_CK(cudaEventRecord(ev_in[k], xstream));
+    };
+    for (int k = 0; k < std::min(2, chunks); ++k) in(k);
+    for (int k = 0; k < chunks; ++k) {
+      LD_CK(cudaStreamWaitEvent(stream, ev_in[k], 0));
+      for (int i = 0; i < nl; ++i) row_mid_chunk(i, k);
+      LD_CK(cudaEventRecord(ev_done[k], stream));
+      if (k + 2 < chunks) in(k + 2);
+      LD_CK(cudaStreamWaitEvent(xstream, ev_done[k], 0));
+      exchange_chunk(false, k, xstream);
+    }
+    LD_CK(cudaEventRecord(ev_back, xstream));
+    LD_CK(cudaStreamWaitEvent(stream, ev_back, 0));
+  }
+  void setup_chunks(int want) {
+    chunks = 1;
+    for (int c = std::max(1, want); c >= 1; --c)
+      if (Hb % c == 0) {
+        chunks = c;
+        break;
+      }
+    if (chunks > 1 && !xstream) {
+      LD_CK(cudaStreamCreateWithFlags(&xstream, cudaStreamNonBlocking));
+      LD_CK(cudaEventCreateWithFlags(&ev_col, cudaEventDisableTiming));
+      LD_CK(cudaEventCreateWithFlags(&ev_back, cudaEventDisableTiming));
+    }
+    while ((int)ev_in.size() < chunks) {
+      cudaEvent_t a, b;
+      LD_CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      LD_CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      ev_in.push_back(a);
+      ev_done.push_back(b);
+    }
+  }
+
   void enqueue_steps(long long n) {
     if (!have_dt) raise(Errc::config_error, "set_dt must be called before stepping");
     if (n <= 0) return;
     const int nl = (int)local.size();
     for (int i = 0; i < nl; ++i) col_entry(i);
     for (long long k = 0; k < n; ++k) {
-      exchange(true);
-      for (int i = 0; i < nl; ++i) row_mid(i);
-      exchange(false);
+      if (chunks > 1) {
+        row_side_pipelined();
+      } else {
+        exchange(true);
+        for (int i = 0; i < nl; ++i) row_mid(i);
+        exchange(false);
+      }
       for (int i = 0; i < nl; ++i) {
         if (k + 1 < n)
           col_mid(i);
@@ -629,6 +744,12 @@ DistSolver::DistSolver(const Lattice& lat, const AntiAliasSet& aa, const Problem
   LD_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
   s.choose_geometry();
   s.upload_twiddles();
+  {
+    // NCCL ranks overlap the exchanges with the row passes in 4 row chunks;
+    // virtual ranks (device copies, nothing to hide) keep one, unless asked
+    const char* e = std::getenv("LATTDSE_DIST_CHUNKS");
+    s.setup_chunks(e ? std::atoi(e) : (opt.rank >= 0 && opt.world > 1 ? 4 : 1));
+  }
   if (s.rank < 0)
     for (int g = 0; g < s.G; ++g) s.local.push_back(g);
   else
@@ -650,7 +771,13 @@ DistSolver::DistSolver(const Lattice& lat, const AntiAliasSet& aa, const Problem
 DistSolver::~DistSolver() {
   if (!p_) return;
   if (p_->stream) cudaStreamSynchronize(p_->stream);
+  if (p_->xstream) cudaStreamSynchronize(p_->xstream);
   if (p_->comm) Nccl::get().CommDestroy(p_->comm);
+  for (auto e : p_->ev_in) cudaEventDestroy(e);
+  for (auto e : p_->ev_done) cudaEventDestroy(e);
+  if (p_->ev_col) cudaEventDestroy(p_->ev_col);
+  if (p_->ev_back) cudaEventDestroy(p_->ev_back);
+  if (p_->xstream) cudaStreamDestroy(p_->xstream);
   if (p_->stream) cudaStreamDestroy(p_->stream);
 }
 

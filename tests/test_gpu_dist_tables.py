@@ -99,3 +99,29 @@ def test_table_peak_memory_scales_with_ranks():
     assert peaks[4] <= 0.62 * peaks[2] and peaks[8] <= 0.62 * peaks[4], peaks
     Df = _dist(lat, cfg.eps, a, b, c, p, cfg.sigma, cfg.dt, 8, norm2, mode="full")
     assert Df.info()["table_peak_bytes"] >= 3.0 * peaks[8]
+
+
+@pytest.mark.parametrize("chunks", [3, 4])
+def test_chunked_overlapped_row_side_identical(chunks, monkeypatch):
+    """The pipelined row side (exchange chunks on their own stream under the
+    row passes of the other chunks) gives bit-identical results to the
+    blocking exchanges: two-level (config 1, 4 ranks) and three-level rows."""
+    cfg = configs.CONFIGS["C1"]
+    lat = configs.lattice(cfg)
+    a, b, c, p = configs.problem(cfg)
+    norm2, _, _ = L.aaset_build(lat, with_vectors=False)
+    monkeypatch.delenv("LATTDSE_DIST_CHUNKS", raising=False)
+    D1 = _dist(lat, cfg.eps, a, b, c, p, cfg.sigma, cfg.dt, 4, norm2)
+    monkeypatch.setenv("LATTDSE_DIST_CHUNKS", str(chunks))
+    Dk = _dist(lat, cfg.eps, a, b, c, p, cfg.sigma, cfg.dt, 4, norm2)
+    D1.step(5)
+    Dk.step(5)
+    assert np.array_equal(D1.get_state().view(np.uint64), Dk.get_state().view(np.uint64))
+    lat3, a3, b3, c3, p3 = configs.small_rank1(4, 8388617, seed=3)
+    monkeypatch.delenv("LATTDSE_DIST_CHUNKS", raising=False)
+    E1 = _dist(lat3, 0.05, a3, b3, c3, p3, 0.1, 1.0 / 128, 2, None)
+    monkeypatch.setenv("LATTDSE_DIST_CHUNKS", str(chunks))
+    Ek = _dist(lat3, 0.05, a3, b3, c3, p3, 0.1, 1.0 / 128, 2, None)
+    E1.step(2)
+    Ek.step(2)
+    assert np.array_equal(E1.get_state().view(np.uint64), Ek.get_state().view(np.uint64))
