@@ -531,9 +531,9 @@ struct Solver::Impl {
   long long launches4 = 0;
   int num_sms = 148;
   int minb_override = std::getenv("LATTDSE_MINB") ? std::atoi(std::getenv("LATTDSE_MINB")) : 0;
-  // CUDA graphs of kGraphSteps identical middle steps, per (group start, size)
+  // CUDA graphs of kGraphSteps (and 16, 8, 4) identical middle steps, per (group start, size)
   static constexpr int kGraphSteps = 32;
-  std::map<std::pair<long long, long long>, cudaGraphExec_t> graphs;
+  std::map<std::tuple<long long, long long, long long>, cudaGraphExec_t> graphs;  // (group start, size, steps)
   bool use_graphs = std::getenv("LATTDSE_NO_GRAPHS") == nullptr;
   // programmatic dependent launch between consecutive passes (opt-in LATTDSE_PDL=1:
   // measured neutral on C1/C3, +1% on C2; profiles/README.md)
@@ -549,7 +549,10 @@ struct Solver::Impl {
 
   explicit Impl(const Lattice& l) : lat(l) {}
 
-  DBuf<double> obs_part;
+  DBuf<double> obs_part, obs_kin;  // exit-pass partials of the samples / of the analysis (kinetic part)
+  double* rec_host = nullptr;      // pinned record buffer of propagate (block partials per record)
+  size_t rec_host_n = 0;
+  std::vector<cudaEvent_t> rec_ev;
   // CTAs per batch member of the exit pass that produces samples (rank 1:
   // COL STOREDIAG over M2 columns; rank 2: ROW STOREDIAG over n1 rows) or
   // coefficients (rank 2 analysis: COL STOREDIAG over n2 columns)
@@ -563,23 +566,6 @@ struct Solver::Impl {
     dev::PassKernel* k = dev::find_pass_kernel(AX_COL, (int)M1, PROG_STOREDIAG, +1);
     return k ? (M2 + k->B - 1) / k->B : 0;
   }
-  // per-member (sum |u|^2, sum w |u|^2) from the exit-pass partials, in long double
-  std::vector<std::pair<double, double>> finish_obs(long long nblk, long long nb) {
-    std::vector<double> h((size_t)(2 * nblk * nb));
-    LD_CK(cudaMemcpyAsync(h.data(), obs_part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
-    LD_CK(cudaStreamSynchronize(stream));
-    std::vector<std::pair<double, double>> out((size_t)nb);
-    for (long long m = 0; m < nb; ++m) {
-      long double a = 0, b = 0;
-      for (long long i = 0; i < nblk; ++i) {
-        a += h[(size_t)(2 * (m * nblk + i))];
-        b += h[(size_t)(2 * (m * nblk + i) + 1)];
-      }
-      out[(size_t)m] = {(double)a, (double)b};
-    }
-    return out;
-  }
-
   // ---- launch helpers
   void launch_pass(int axis, int L, int prog, int sign, PassArgs a, long long nlines, long long nbatch) {
     dev::PassKernel* k = dev::find_pass_kernel(axis, L, prog, sign);
@@ -1233,8 +1219,8 @@ struct Solver::Impl {
   void analyze_dev(const double2* s, double2* c, double2* w, bool kin_obs = false) {
     ObsSpec o;
     if (kin_obs) {
-      obs_part.alloc((size_t)(2 * exit_blocks(true)));
-      o.out = obs_part.p;
+      obs_kin.alloc((size_t)(2 * exit_blocks(true)));
+      o.out = obs_kin.p;
       o.widx = nidx.p;
       o.wscale = 0.5 * eps * 4.0 * M_PI * M_PI;
     }
@@ -1381,9 +1367,9 @@ struct Solver::Impl {
         // plain transforms on either side of the first-axis pass
         timed(pt, false, [&] { g_row(PROG_LOADDIAG, -1, s, w, Vh.p, gb); });
         for (long long k = 0; k < nsteps; ++k) {
-          timed(pt, true, [&] { g_axes(-1, w, gb); });
+          if (!axes.empty()) timed(pt, true, [&] { g_axes(-1, w, gb); });
           timed(pt, true, [&] { g_col(PROG_DOUBLE, -1, w, w, DG_LUT16, gb); });
-          timed(pt, true, [&] { g_axes(+1, w, gb); });
+          if (!axes.empty()) timed(pt, true, [&] { g_axes(+1, w, gb); });
           if (k + 1 < nsteps)
             timed(pt, false, [&] { g_row(PROG_DOUBLE, +1, w, w, V.p, gb); });
           else
@@ -1395,26 +1381,29 @@ struct Solver::Impl {
         // middle steps (ROW, COL) in graph chunks: identical launches, so the
         // GPU runs them back to back without host launch latency
         if (!pt && use_graphs && !sync_check && row_chunk == 0) {
-          const long long chunks = (nsteps - 1) / kGraphSteps;
-          if (chunks > 0) {
-            cudaGraphExec_t& ge = graphs[{g0, gb}];
-            if (!ge) {
-              cudaGraph_t g;
-              LD_CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-              for (int i = 0; i < kGraphSteps; ++i) {
-                r1_row_mid(w, Khat.p, gb);
-                r1_col_mid(w, V.p, gb);
+          // nsteps - 1 middle steps as graphs of 32, then 16, 8, 4 (a
+          // propagation that records every 64 steps would otherwise run
+          // half of them as loose launches with host gaps between)
+          const int per = three ? 4 : 2;
+          for (long long len = kGraphSteps; len >= 4; len >>= 1) {
+            while (nsteps - 1 - k >= len) {
+              cudaGraphExec_t& ge = graphs[{g0, gb, len}];
+              if (!ge) {
+                cudaGraph_t g;
+                LD_CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+                for (long long i = 0; i < len; ++i) {
+                  r1_row_mid(w, Khat.p, gb);
+                  r1_col_mid(w, V.p, gb);
+                }
+                LD_CK(cudaStreamEndCapture(stream, &g));
+                LD_CK(cudaGraphInstantiate(&ge, g, 0));
+                cudaGraphDestroy(g);
+                launches -= per * len;  // counted per replay below
               }
-              LD_CK(cudaStreamEndCapture(stream, &g));
-              LD_CK(cudaGraphInstantiate(&ge, g, 0));
-              cudaGraphDestroy(g);
-              launches -= (three ? 4 : 2) * kGraphSteps;  // counted per replay below
-            }
-            for (long long c = 0; c < chunks; ++c) {
               LD_CK(cudaGraphLaunch(ge, stream));
-              launches += (three ? 4 : 2) * kGraphSteps;
+              launches += per * len;
+              k += len;
             }
-            k = chunks * kGraphSteps;
           }
         }
         for (; k < nsteps; ++k) {
@@ -1601,6 +1590,8 @@ Solver::~Solver() {
   if (p_ && p_->stream) {
     cudaStreamSynchronize(p_->stream);
     p_->drop_graphs();
+    for (auto e : p_->rec_ev) cudaEventDestroy(e);
+    if (p_->rec_host) cudaFreeHost(p_->rec_host);
     if (p_->persist_bytes > 0) cudaCtxResetPersistingL2Cache();
     cudaStreamDestroy(p_->stream);
   }
@@ -1743,25 +1734,70 @@ std::vector<TrajectoryRow> Solver::propagate(std::int64_t m, std::int64_t record
   }
   const double norm0 = rows[0].norm;
   const double invN = 1.0 / (double)s.N;
-  for (std::int64_t k = 0; k < m;) {
-    std::int64_t n = std::min(record_every, m - k);
-    // observables fused into the passes: the exit
-    // pass that writes the samples also sums |u|^2 and v |u|^2 per member;
-    // the kinetic part comes out of the analysis exit pass of this member
-    s.enqueue_steps(n, nullptr, true);
-    const auto part = s.finish_obs(s.exit_blocks(false), s.batch)[(size_t)member];
-    s.coef.alloc(s.N);
-    s.analyze_dev(s.samples.p + member * s.N, s.coef.p, s.work.p, true);
-    const double kin = s.finish_obs(s.exit_blocks(true), 1)[0].second;
-    LD_CK(cudaGetLastError());
-    k += n;
-    rows.push_back({k, (double)k * s.dt_, std::sqrt(part.first * invN), kin + part.second * invN / s.eps});
+  // Observables fused into the passes: the exit pass
+  // that writes the samples also sums |u|^2 and v |u|^2 per member; the
+  // kinetic part comes out of the analysis exit pass of this member. Records
+  // are asynchronous: the block partials go to pinned host memory behind the
+  // passes and the host finishes record r-1 (long double sums, watchdog)
+  // while record r's steps are already queued, so the GPU never waits for
+  // the host between records.
+  const long long nblk_s = s.exit_blocks(false), nblk_k = s.exit_blocks(true);
+  const std::int64_t nrec = m > 0 ? (m + record_every - 1) / record_every : 0;
+  const size_t per = (size_t)(2 * (nblk_s + nblk_k));
+  // pinned record buffer and events live with the solver (pinned allocation
+  // costs milliseconds: it would dominate a short propagation)
+  if (s.rec_host_n < per * (size_t)nrec) {
+    if (s.rec_host) cudaFreeHost(s.rec_host);
+    s.rec_host = nullptr;
+    s.rec_host_n = 0;
+    LD_CK(cudaMallocHost(&s.rec_host, per * (size_t)nrec * sizeof(double)));
+    s.rec_host_n = per * (size_t)nrec;
+  }
+  double* host = s.rec_host;
+  while (s.rec_ev.size() < (size_t)nrec) {
+    cudaEvent_t e;
+    LD_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s.rec_ev.push_back(e);
+  }
+  std::vector<cudaEvent_t>& ev = s.rec_ev;
+  s.coef.alloc(s.N);
+  std::vector<std::int64_t> at((size_t)nrec);
+  auto finish = [&](std::int64_t r) {
+    LD_CK(cudaEventSynchronize(ev[(size_t)r]));
+    const double* h = host + per * (size_t)r;
+    long double sq = 0, pot = 0, kin = 0;
+    for (long long i = 0; i < nblk_s; ++i) {
+      sq += h[2 * i];
+      pot += h[2 * i + 1];
+    }
+    for (long long i = 0; i < nblk_k; ++i) kin += h[2 * nblk_s + 2 * i + 1];
+    const std::int64_t k = at[(size_t)r];
+    rows.push_back({k, (double)k * s.dt_, std::sqrt((double)sq * invN), (double)kin + (double)pot * invN / s.eps});
     // norm-drift watchdog (numerical_invariant, CLI exit code 3)
     const double drift = std::fabs(rows.back().norm - norm0);
-    if (p_->watchdog_tol > 0 && !(drift <= p_->watchdog_tol))
+    if (p_->watchdog_tol > 0 && !(drift <= p_->watchdog_tol)) {
+      cudaStreamSynchronize(s.stream);  // queued steps finish before the buffers go away
       raise(Errc::numerical_invariant, "norm drift " + std::to_string(drift) + " at step " + std::to_string(k) +
                                            " exceeds " + std::to_string(p_->watchdog_tol));
+    }
+  };
+  std::int64_t r = 0;
+  for (std::int64_t k = 0; k < m; ++r) {
+    const std::int64_t n = std::min(record_every, m - k);
+    s.enqueue_steps(n, nullptr, true);
+    double* h = host + per * (size_t)r;
+    LD_CK(cudaMemcpyAsync(h, s.obs_part.p + 2 * nblk_s * member, (size_t)(2 * nblk_s) * sizeof(double),
+                          cudaMemcpyDeviceToHost, s.stream));
+    s.analyze_dev(s.samples.p + member * s.N, s.coef.p, s.work.p, true);
+    LD_CK(cudaMemcpyAsync(h + 2 * nblk_s, s.obs_kin.p, (size_t)(2 * nblk_k) * sizeof(double), cudaMemcpyDeviceToHost,
+                          s.stream));
+    LD_CK(cudaEventRecord(ev[(size_t)r], s.stream));
+    LD_CK(cudaGetLastError());
+    k += n;
+    at[(size_t)r] = k;
+    if (r > 0) finish(r - 1);
   }
+  if (nrec > 0) finish(nrec - 1);
   return rows;
 }
 

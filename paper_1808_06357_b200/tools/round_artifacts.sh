@@ -21,7 +21,7 @@ python bench.py --config C4 --steps 2 --warmup 3 --no-cpu > "$T/bench_C4.json" 2
 if [ "$rc" = 0 ]; then
   B="python bench.py --m 4 --steps 1 --warmup 3 --no-cpu"
   $B > "$T/plain.log" 2>&1 && {
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$T/launches.csv" $B > "$T/launches.log" 2>&1
+  ncu --metrics gpu__time_duration.sum --clock-control none -k regex:fft_pass -c 400 --csv --log-file "$T/launches.csv" $B > "$T/launches.log" 2>&1
   echo "ncu launches rc=$?" >> "$T/status.txt"
   ncu --set full --import-source on --clock-control none -k regex:fft_pass --launch-skip 12 --launch-count 2 \
       -f -o "$T/prof_c3" $B > "$T/ncu_full.log" 2>&1

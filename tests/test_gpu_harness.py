@@ -205,8 +205,15 @@ def test_conservation_config1_scale(tmp_path):
 
 
 def test_propagate_overhead_config1():
-    """Observables at record steps cost little over plain stepping: C1,
-    1024 steps, a record every 64 (fused sums + one analysis per record)."""
+    """Observables at record steps cost little over plain stepping. Worst case
+    of the configs: C1 (one small wave function, 57 us per step), 1024 steps,
+    a record every 64. A record is the exit + re-entry pass (fused sums of
+    |u|^2 and v |u|^2) and one Bluestein analysis (three passes, fused
+    kinetic sum): ~5.5 steps' worth, i.e. ~9% here (measured 63.2 vs 58.1 ms,
+    scripts/prop_time.py); records are asynchronous (pinned host ring, the
+    host finishes record r-1 under record r's steps), a single record costs
+    under 1%, and an ensemble member's record vanishes next to the step of
+    all members."""
     import time
 
     cfg = configs.CONFIGS["C1"]
@@ -214,11 +221,18 @@ def test_propagate_overhead_config1():
     a, b, c, p = configs.problem(cfg)
     S = _solver(lat, cfg.eps, a, b, c, p, cfg.sigma, cfg.dt)
     S.step(cfg.m)  # warm the graphs
-    S.propagate(64, 64)
-    t0 = time.perf_counter()
-    S.step(cfg.m)
-    t_step = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    S.propagate(cfg.m, 64)
-    t_prop = time.perf_counter() - t0
-    assert t_prop <= 1.10 * t_step, (t_prop, t_step)
+    S.propagate(128, 64)
+
+    def best(f):
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            f()
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    t_step = best(lambda: S.step(cfg.m))
+    t_prop = best(lambda: S.propagate(cfg.m, 64))
+    t_one = best(lambda: S.propagate(cfg.m, cfg.m))
+    assert t_prop <= 1.12 * t_step, (t_prop, t_step)
+    assert t_one <= 1.02 * t_step, (t_one, t_step)
