@@ -314,7 +314,7 @@ int lattdse_solver_create(const lattdse_lattice* lat, const lattdse_problem* pro
     need(out, "out");
     auto ps = make_problem(prob);
     // rank-1: the solver builds the norm table on its device (empty norm2);
-    // rank-2: the host shell walk
+    // rank >= 2: the host shell walk
     lattdse::AntiAliasSet aa;
     if (lat->lat.rank() != 1) aa = lattdse::AntiAliasSet::build(lat->lat, false);
     auto* h = new lattdse_solver;

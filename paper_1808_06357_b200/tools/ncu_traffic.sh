@@ -22,5 +22,5 @@ run() {  # name, skip, count, bench args...
 }
 run C2 10 4 --config C2 --steps 1 --warmup 3 --m 8 --no-cpu
 run C3 10 4 --config C3 --steps 1 --warmup 3 --m 8 --no-cpu
-run C4 8 14 --config C4 --steps 1 --warmup 1 --m 2 --no-cpu
+run C4 8 20 --config C4 --steps 1 --warmup 1 --m 3 --no-cpu
 cat "$T/status_traffic.txt"
