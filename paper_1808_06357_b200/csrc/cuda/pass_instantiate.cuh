@@ -94,23 +94,25 @@ template <int AXIS, int L> struct Geometry4 {
 template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
   using G = Geometry<AXIS, L>;
   PassKernel k;
-  k.fn = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN>);
   k.B = G::B;
   k.NT = G::NT;
   k.smem = lattdse_dev::SmemGeom<L, G::B>::bytes;
   k.nst = lattdse_dev::Plan<L>::nst;
   for (int s = 0; s < k.nst && s < 16; ++s) k.radix[s] = lattdse_dev::Plan<L>::radix(s);
   if constexpr (PROG == lattdse_dev::PROG_DOUBLE) {
-    k.fn_mb[1] = k.fn;
-    k.fn_mb[2] = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN, 2>);
-    k.fn_mb[3] = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN, 3>);
-    k.fn_mb[4] = nullptr;  // measured never best (spills); not instantiated to keep the library small
-    // measured on C1 (profiles/README.md): 3 resident CTAs/SM balance register
-    // caps (small L1-resident spills) against occupancy for 5-10 warp CTAs
-    // ROW: 3 CTAs/SM; COL (four-step twiddle math in the fused stages) keeps
-    // more registers at 2 CTAs/SM
-    // ROW lines of 4096 (radix-16 stages) spill heavily under the 3-CTA cap
-    k.default_mb = G::wide_col ? 1 : (G::NT > 320 ? 2 : (AXIS == lattdse_dev::AX_ROW && L < 4096 ? 3 : 2));
+    // resident CTAs per SM the double program is compiled for (its register
+    // cap), measured on C1 / C2 (profiles/README.md): ROW 3 (small L1-resident
+    // spills against occupancy for 5-10 warp CTAs); COL (four-step twiddle
+    // math in the fused stages) and CTAs above 320 threads 2; ROW lines of
+    // 4096 (radix-16 stages) spill heavily under the 3-CTA cap: 2; the wide
+    // 4096-long COL tile 1. Only this variant is instantiated (the 1 / 2 / 3
+    // sweep of round 1 tripled the library for a debugging knob).
+    constexpr int mb = G::wide_col ? 1 : (G::NT > 320 ? 2 : (AXIS == lattdse_dev::AX_ROW && L < 4096 ? 3 : 2));
+    k.fn = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN, mb>);
+    k.fn_mb[mb] = k.fn;
+    k.default_mb = mb;
+  } else {
+    k.fn = reinterpret_cast<const void*>(&lattdse_dev::fft_pass_kernel<AXIS, L, G::B, G::NT, PROG, SIGN>);
   }
   if constexpr (LATTDSE_BUILD_PASS4 && PROG == lattdse_dev::PROG_DOUBLE && Geometry4<AXIS, L>::ok) {
     using G4 = Geometry4<AXIS, L>;

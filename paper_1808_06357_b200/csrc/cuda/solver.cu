@@ -530,7 +530,6 @@ struct Solver::Impl {
   int pass4_pf = std::getenv("LATTDSE_PASS4_PF") ? std::atoi(std::getenv("LATTDSE_PASS4_PF")) : 0;  // L2 prefetch distance, tiles
   long long launches4 = 0;
   int num_sms = 148;
-  int minb_override = std::getenv("LATTDSE_MINB") ? std::atoi(std::getenv("LATTDSE_MINB")) : 0;
   // CUDA graphs of kGraphSteps (and 16, 8, 4) identical middle steps, per (group start, size)
   static constexpr int kGraphSteps = 32;
   std::map<std::tuple<long long, long long, long long>, cudaGraphExec_t> graphs;  // (group start, size, steps)
@@ -577,7 +576,7 @@ struct Solver::Impl {
     }
     const void* fn = k->fn;
     if (prog == PROG_DOUBLE) {
-      const int mb = minb_override > 0 ? minb_override : k->default_mb;
+      const int mb = k->default_mb;
       if (mb >= 1 && mb <= 4 && k->fn_mb[mb]) fn = k->fn_mb[mb];
     }
     int smem = k->smem;
