@@ -44,8 +44,31 @@ template <int L> struct P4Seq {
   static constexpr bool inner(int q) { return q > 0 && q != nst - 1 && q < 2 * nst - 2; }
   static constexpr int P(int q) { return inner(q) ? Ns(q) * R(q) : 0; }  // skew period of the buffer position q writes
   static constexpr int C(int q) { return inner(q) ? ((Ns(q) * (1 - R(q))) % 8 + 8) % 8 : 0; }
+  // Power-of-two style plans (first or last radix a multiple of 4): their
+  // Ns = 1 stage writes j R + r collide 4- to 8-fold, so every buffer is
+  // swizzled by one slot per 16, phys(i) = i + i / 16 (as the generic kernels
+  // do). Addresses stay "base + compile-time offset": phys(base + off) =
+  // phys(base) + phys(off) whenever the low four bits do not carry, which
+  // holds for every access of such a plan -- reads j + r T with 16 | T,
+  // writes (j - k) R + k + r Ns with Ns = 1 and R in {4, 8, 16} (base a
+  // multiple of R, off = r < R), 16 | Ns, or Ns = 8 with k < 8 (off = 8 r).
+  static constexpr bool swz = (R(0) % 4 == 0 || R(nst - 1) % 4 == 0) && L >= 64;
+  static constexpr bool swz_ok() {
+    if (!swz) return true;
+    for (int q = 0; q < 2 * nst - 1; ++q) {
+      const int r = R(q), ns = Ns(q), t = L / r;
+      if (q > 0 && t % 16 != 0) return false;                                  // reads of stage q
+      if (C(q) != 0) return false;                                              // never together with the skew
+      if (q != nst - 1 && q != 2 * nst - 2) {                                   // Stockham write of stage q
+        if (ns == 1 ? !(r == 4 || r == 8 || r == 16) : !(ns % 16 == 0 || ns == 8)) return false;
+      }
+    }
+    const int rl = R(nst - 1);  // the fused mid stage writes with the reversed plan's stage 0 (Ns = 1)
+    return rl == 4 || rl == 8 || rl == 16;
+  }
+  static constexpr int ph(int i) { return swz ? i + i / 16 : i; }
   static constexpr int extent() {
-    int m = L;
+    int m = ph(L - 1) + 1;
     for (int q = 0; q < 2 * nst - 1; ++q)
       if (P(q) > 0 && L + C(q) * (L / P(q)) > m) m = L + C(q) * (L / P(q));
     return m;
@@ -79,6 +102,7 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
   using SQ = P4Seq<L>;
   static constexpr int BG = G::BG, LS = G::LS, nst = Plan<L>::nst;
   static_assert(nst >= 2, "pass4 needs at least two stages");
+  static_assert(P4Seq<L>::swz_ok(), "plan needs a swizzle this kernel cannot keep affine");
 
   const PassArgs& a;
   double2* sm;   // buffer 0; buffer 1 at sm + tile when ping-ponging
@@ -87,6 +111,7 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
   double2* gout;
   int line0;
 
+  __device__ __forceinline__ static int pb(int x) { return SQ::swz ? x + (x >> 4) : x; }  // swizzled runtime base
   template <int P_, int C_> __device__ __forceinline__ static int skew(int j) {
     if constexpr (C_ == 0) return 0;
     else return C_ * (j / P_);
@@ -176,9 +201,9 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
       for (int l = 0; l < LPT; ++l) {
         if (TW) fourstep<R, true>(bgs[t] + l * BG, js[t], v[t][l]);
         DFT<R, SIGN1>::run(v[t][l]);
-        double2* o = buf(1) + (bgs[t] + l * BG) * LS + js[t] * R;
+        double2* o = buf(1) + (bgs[t] + l * BG) * LS + pb(js[t] * R);
 #pragma unroll
-        for (int r = 0; r < R; ++r) o[r] = v[t][l][r];
+        for (int r = 0; r < R; ++r) o[SQ::ph(r)] = v[t][l][r];
       }
     }
   }
@@ -200,9 +225,9 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
       map(q, T, bgs[t], js[t]);
 #pragma unroll
       for (int l = 0; l < LPT; ++l) {
-        const double2* p = buf(Q) + (bgs[t] + l * BG) * LS + js[t] + skew<Pr, Cr>(js[t]);
+        const double2* p = buf(Q) + (bgs[t] + l * BG) * LS + pb(js[t]) + skew<Pr, Cr>(js[t]);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[t][l][r] = p[r * Tr];
+        for (int r = 0; r < R; ++r) v[t][l][r] = p[SQ::ph(r * Tr)];
       }
     }
     if (!G::pp) __syncthreads();  // in place: every read before any write
@@ -216,9 +241,9 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
       for (int l = 0; l < LPT; ++l) {
         apply_pow<R, SIGN>(pw, v[t][l]);
         DFT<R, SIGN>::run(v[t][l]);
-        double2* o = buf(Q + 1) + (bgs[t] + l * BG) * LS + (j - k) * R + k + skew<Ns, Cw>(j);
+        double2* o = buf(Q + 1) + (bgs[t] + l * BG) * LS + pb((j - k) * R + k) + skew<Ns, Cw>(j);
 #pragma unroll
-        for (int r = 0; r < R; ++r) o[r * Ns] = v[t][l][r];
+        for (int r = 0; r < R; ++r) o[SQ::ph(r * Ns)] = v[t][l][r];
       }
     }
   }
@@ -260,9 +285,9 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
       map(q, T, bgs[t], js[t]);
 #pragma unroll
       for (int l = 0; l < LPT; ++l) {
-        const double2* p = buf(Q) + (bgs[t] + l * BG) * LS + js[t] + skew<Pr, Cr>(js[t]);
+        const double2* p = buf(Q) + (bgs[t] + l * BG) * LS + pb(js[t]) + skew<Pr, Cr>(js[t]);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[t][l][r] = p[r * Tr];
+        for (int r = 0; r < R; ++r) v[t][l][r] = p[SQ::ph(r * Tr)];
       }
     }
     if (!G::pp) __syncthreads();
@@ -282,9 +307,9 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
 #pragma unroll
         for (int r = 0; r < R; ++r) v[t][l][r] = c_mul(v[t][l][r], dg[r]);
         DFT<R, -SIGN1>::run(v[t][l]);  // stage 0 of the reversed plan (Ns = 1)
-        double2* o = buf(Q + 1) + b * LS + j * R;
+        double2* o = buf(Q + 1) + b * LS + pb(j * R);
 #pragma unroll
-        for (int r = 0; r < R; ++r) o[r] = v[t][l][r];
+        for (int r = 0; r < R; ++r) o[SQ::ph(r)] = v[t][l][r];
       }
     }
   }
@@ -307,9 +332,9 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
 #pragma unroll
       for (int l = 0; l < LPT; ++l) {
         double2 v[R];
-        const double2* p = buf(Q) + (bg + l * BG) * LS + j + skew<Pr, Cr>(j);
+        const double2* p = buf(Q) + (bg + l * BG) * LS + pb(j) + skew<Pr, Cr>(j);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = p[r * Tr];
+        for (int r = 0; r < R; ++r) v[r] = p[SQ::ph(r * Tr)];
         apply_pow<R, -SIGN1>(pw, v);
         DFT<R, -SIGN1>::run(v);
         if (TW) fourstep<R, false>(bg + l * BG, j, v);

@@ -42,21 +42,23 @@ template <int AXIS, int L> struct Geometry {
 //  COL: more, smaller CTAs beat wider tiles -- L <= 648: four adjacent
 //       columns (64-byte row segments) in place, COL 486 four CTAs of 224
 //       threads 348 vs two CTAs of eight columns 366 vs v1 441; longer
-//       columns two per CTA, with two stage buffers while they fit 90 KB
-//       (config 1, COL 1296: 35.0 vs 39.0 in place vs v1 39.7);
+//       columns two per CTA (also 4096: 262 vs 338 for one column), with
+//       two stage buffers while they fit 90 KB (config 1, COL 1296: 35.0 vs
+//       39.0 in place vs v1 39.7);
 //  NT covers the busiest stage unless a narrower CTA running that stage in
 //  two rounds wastes fewer thread slots; resident CTAs per SM as ~96 (two
 //  buffers) or ~72 (in place) registers per thread and the shared memory
 //  allow (ROW 1080: 5 CTAs of 128 threads 271, 6 CTAs at 80 registers 293).
-// Plans whose first or last radix is a multiple of 4 stay on the v1 kernels
-// (their Ns = 1 stage writes conflict 4- to 8-fold without v1's swizzled
-// slots: ROW 4096 259 vs v1 220, COL 4096 296 vs 304 on config 2).
+// Plans whose first or last radix is a multiple of 4 run with swizzled
+// slots (P4Seq::swz; ROW 4096 163 vs 259 unswizzled vs v1 216, COL 4096 two
+// columns 262 vs v1 303 on config 2, ROW 2048 139 vs v1 219); the few such
+// plans the swizzle cannot keep affine (512, 1024: a radix-2 / 4 end stage
+// behind radix 16) stay on the v1 kernels.
 template <int AXIS, int L> struct Geometry4 {
   using P = lattdse_dev::Plan<L>;
-  static constexpr bool ok = P::nst >= 2 && L >= 64 && P::radix(0) % 4 != 0 && P::radix(P::nst - 1) % 4 != 0;
-  static constexpr int B = AXIS == lattdse_dev::AX_ROW ? (L >= 512 ? 1 : (L >= 256 ? 2 : 256 / L * 2))
-                                                       : (L <= 648 ? 4 : (L <= 2592 ? 2 : 1));
-  static constexpr bool PP = 2 * B * L * 16 <= (AXIS == lattdse_dev::AX_ROW ? 72 : (L <= 648 ? 0 : 90)) * 1024;
+  static constexpr bool row = AXIS == lattdse_dev::AX_ROW;
+  static constexpr bool ok = P::nst >= 2 && L >= 64 && lattdse_dev::P4Seq<L>::swz_ok();
+  static constexpr int B = row ? (L >= 512 ? 1 : (L >= 256 ? 2 : 256 / L * 2)) : (L <= 648 ? 4 : 2);
   // threads: the multiple of 32 with the fewest thread slots over the stage
   // sequence (a stage of t tasks runs ceil(t / NT) rounds of NT threads,
   // each task R elements of work; the fused mid stage runs once with two
@@ -85,10 +87,32 @@ template <int AXIS, int L> struct Geometry4 {
     return best;
   }
   static constexpr int NT = pick_nt();
-  static constexpr int smem = lattdse_dev::P4Geom<AXIS, L, B, 1, PP>::bytes;
-  static constexpr int by_regs = 65536 / (NT * (PP ? 96 : 72)) > 0 ? 65536 / (NT * (PP ? 96 : 72)) : 1;
-  static constexpr int by_smem = (227 * 1024) / (smem + 1024) > 0 ? (227 * 1024) / (smem + 1024) : 1;
+  // registers per thread the kernel is capped to (resident CTAs by registers):
+  // radix-16 end stages 128, else 96 with two stage buffers or a radix >= 15
+  // anywhere, 72 in place with small radices
+  static constexpr bool big = P::radix(0) >= 16 || P::radix(P::nst - 1) >= 16;
+  static constexpr int max_radix() {
+    int m = 0;
+    for (int s = 0; s < P::nst; ++s) m = P::radix(s) > m ? P::radix(s) : m;
+    return m;
+  }
+  static constexpr int ip_budget = big ? 128 : (max_radix() >= 15 ? 96 : 72);
+  static constexpr int fit(int bytes) { return (227 * 1024) / (bytes + 1024) > 0 ? (227 * 1024) / (bytes + 1024) : 1; }
+  static constexpr int regs_ctas(int budget) { return 65536 / (NT * budget) > 0 ? 65536 / (NT * budget) : 1; }
+  static constexpr int bytes_pp = lattdse_dev::P4Geom<AXIS, L, B, 1, true>::bytes;
+  static constexpr int bytes_ip = lattdse_dev::P4Geom<AXIS, L, B, 1, false>::bytes;
+  // two stage buffers (one barrier per stage) when they do not cost resident
+  // CTAs: ROW while both fit 72 KB and shared memory still holds as many
+  // CTAs as the registers allow (ROW 2048: in place at 4 CTAs 139 us, two
+  // buffers at 3 CTAs 180 us over 4 x 2048 lines); COL above 648 while both
+  // fit 90 KB (config 1, COL 1296: 35.0 vs 39.0 us), short COL lines in place
+  static constexpr bool PP = row ? (bytes_pp <= 72 * 1024 && fit(bytes_pp) >= regs_ctas(big ? 128 : 96))
+                                 : (L > 648 && bytes_pp <= 90 * 1024);
+  static constexpr int smem = PP ? bytes_pp : bytes_ip;
+  static constexpr int by_regs = regs_ctas(PP ? (big ? 128 : 96) : ip_budget);
+  static constexpr int by_smem = fit(smem);
   static constexpr int MB = by_regs < by_smem ? by_regs : by_smem;
+  static_assert(smem <= 227 * 1024, "pass4 tile exceeds shared memory");
 };
 
 template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
