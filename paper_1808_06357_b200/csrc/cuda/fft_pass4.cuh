@@ -91,7 +91,8 @@ template <int AXIS, int L, int B, int LPT, bool PP> struct P4Geom {
   static constexpr int tile = B * LS;
   static constexpr bool pp = PP;
   static constexpr int R0 = Plan<L>::radix(0);
-  static constexpr int tw_slots = AXIS == AX_COL ? B * R0 : 0;
+  static constexpr int Rl = Plan<L>::radix(Plan<L>::nst - 1);
+  static constexpr int tw_slots = AXIS == AX_COL ? B * (R0 > Rl ? R0 : Rl) : 0;  // column twiddle powers (first or last radix)
   static constexpr int bytes = (pp ? 2 : 1) * tile * 16 + tw_slots * 16;
 };
 
@@ -110,6 +111,7 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
   const double2* gin;
   double2* gout;
   int line0;
+  long long twm = 1;  // four-step twiddles of a length M / twm (rows of a three-level view): W_M^(twm t)
 
   __device__ __forceinline__ static int pb(int x) { return SQ::swz ? x + (x >> 4) : x; }  // swizzled runtime base
   template <int P_, int C_> __device__ __forceinline__ static int skew(int j) {
@@ -164,7 +166,7 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
   }
   // four-step twiddles of task j, line b (elements j + r T0): base * twp[b][r]
   template <int R, bool CONJ> __device__ __forceinline__ void fourstep(int b, int j, double2 (&v)[R]) const {
-    const double2 base = twid((long long)(line0 + b) * j);
+    const double2 base = twid((long long)(line0 + b) * twm * j);
     const double2* p = twp + b * R;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -174,7 +176,7 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
   }
 
   // ---- stage 0 of the first transform: global -> (conj four-step) -> DFT -> smem
-  __device__ __forceinline__ void first_stage(int tid) const {
+  template <bool PRE = TW> __device__ __forceinline__ void first_stage(int tid) const {
     using P = PlanX<L, false>;
     constexpr int R = P::radix(0), T = L / R, TASKS = BG * T, TPT = (TASKS + NT - 1) / NT;
     double2 v[TPT][LPT][R];
@@ -192,14 +194,14 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
         for (int r = 0; r < R; ++r) v[t][l][r] = p[r * st];
       }
     }
-    if (TW) __syncthreads();  // twp ready (the loads above are already in flight)
+    if (PRE) __syncthreads();  // twp ready (the loads above are already in flight)
 #pragma unroll
     for (int t = 0; t < TPT; ++t) {
       const int q = tid + t * NT;
       if (TASKS % NT != 0 && q >= TASKS) break;
 #pragma unroll
       for (int l = 0; l < LPT; ++l) {
-        if (TW) fourstep<R, true>(bgs[t] + l * BG, js[t], v[t][l]);
+        if (PRE) fourstep<R, true>(bgs[t] + l * BG, js[t], v[t][l]);
         DFT<R, SIGN1>::run(v[t][l]);
         double2* o = buf(1) + (bgs[t] + l * BG) * LS + pb(js[t] * R);
 #pragma unroll
@@ -345,6 +347,50 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
     }
   }
 
+  // ---- single transform (three-level inner passes): last stage of the
+  // forward plan, smem -> twiddle -> DFT -> (four-step) -> global
+  template <int SIGN, bool POST> __device__ __forceinline__ void final_stage(int tid) const {
+    using P = PlanX<L, false>;
+    constexpr int Q = nst - 1, S = nst - 1, R = P::radix(S), Ns = P::ns(S), T = L / R, TASKS = BG * T,
+                  TPT = (TASKS + NT - 1) / NT;
+    static_assert(T == Ns, "last stage covers j + r*T");
+    constexpr int Pr = SQ::P(Q - 1), Cr = SQ::C(Q - 1), Tr = Cr ? T + Cr * (T / Pr) : T;
+    static_assert(Cr == 0 || T % Pr == 0, "reader stride spans whole skew blocks");
+#pragma unroll
+    for (int t = 0; t < TPT; ++t) {
+      const int q = tid + t * NT;
+      if (TASKS % NT != 0 && q >= TASKS) break;
+      int bg, j;
+      map(q, T, bg, j);
+      const Pow<R> pw = stage_pow<R, Ns, false, S>(j);
+      const long long st = gstep(T);
+#pragma unroll
+      for (int l = 0; l < LPT; ++l) {
+        double2 v[R];
+        const double2* p = buf(Q) + (bg + l * BG) * LS + pb(j) + skew<Pr, Cr>(j);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = p[SQ::ph(r * Tr)];
+        apply_pow<R, SIGN>(pw, v);
+        DFT<R, SIGN>::run(v);
+        if (POST) fourstep<R, false>(bg + l * BG, j, v);
+        double2* o = gout + gpos(bg + l * BG, j);
+#pragma unroll
+        for (int r = 0; r < R; ++r) o[r * st] = v[r];
+      }
+    }
+  }
+  template <int SIGN, bool PRE, bool POST> __device__ __forceinline__ void run_single(int tid) const {
+    static_assert(SIGN == SIGN1, "single transforms run in the kernel's sign");
+    first_stage<PRE>(tid);
+    __syncthreads();  // stage buffer written; POST: also the twiddle powers of the output side
+    sfor<nst - 2>([&](auto sc) {
+      constexpr int s = decltype(sc)::value + 1;
+      inner_stage<s, false, SIGN, s>(tid);
+      __syncthreads();
+    });
+    final_stage<SIGN, POST>(tid);
+  }
+
   __device__ __forceinline__ void run(int tid) const {
     first_stage(tid);
     __syncthreads();
@@ -395,7 +441,7 @@ __global__ void __launch_bounds__(NT, MINB) fft_pass4_kernel(const __grid_consta
     }
   }
   double2* twp = lattdse_smem4 + (G::pp ? 2 : 1) * G::tile;
-  K k{a, lattdse_smem4, twp, a.in + bat * a.in_bstride, a.out + bat * a.out_bstride, line0};
+  K k{a, lattdse_smem4, twp, a.in + bat * a.in_bstride, a.out + bat * a.out_bstride, line0, 1};
   if (TW) {
     // twp[b][r] = W^(col_b * T0 * r): the powers every task of column b needs
     constexpr int R0 = G::R0, T0 = L / R0;
@@ -405,6 +451,36 @@ __global__ void __launch_bounds__(NT, MINB) fft_pass4_kernel(const __grid_consta
     }
   }
   k.run(tid);
+}
+
+
+// Single-transform pass of the plain COL layout with four-step twiddles on
+// one side (the three-level inner passes: FFT_Ma then x W_M2, or x conj W_M2
+// then IFFT_Ma, inside every row of the M1 x M2 view; blockIdx.y = row).
+// PRE: conjugate twiddles at the load (elements j + r T0 of the first
+// stage); POST: twiddles at the store (elements j + r T of the last stage).
+template <int L, int B, bool PP, int NT, int SIGN, bool PRE, int MINB>
+__global__ void __launch_bounds__(NT, MINB) fft_single4_kernel(const __grid_constant__ PassArgs a) {
+  using K = Pass4<AX_COL, L, B, 1, PP, NT, SIGN, true, DG_NONE>;
+  using G = typename K::G;
+  extern __shared__ double2 lattdse_smem4[];
+  const int tid = threadIdx.x;
+  const int line0 = (int)blockIdx.x * B;
+  const long long bat = blockIdx.y;
+  double2* twp = lattdse_smem4 + (G::pp ? 2 : 1) * G::tile;
+  K k{a, lattdse_smem4, twp, a.in + bat * a.in_bstride, a.out + bat * a.out_bstride, line0, a.tw_mul > 1 ? a.tw_mul : 1};
+  // powers of the column twiddles for the side that carries them: the first
+  // stage's elements j + r T0 (PRE) or the last stage's j + r T (POST)
+  constexpr int Rt = PRE ? G::R0 : Plan<L>::radix(Plan<L>::nst - 1), Tt = L / Rt;
+  static_assert(B * Rt <= G::tw_slots, "twiddle slots");
+  for (int i = tid; i < B * Rt; i += NT) {
+    const int b = i / Rt, r = i - b * Rt;
+    twp[i] = k.twid((long long)(line0 + b) * k.twm * (Tt * r));
+  }
+  if (PRE)
+    k.template run_single<SIGN, true, false>(tid);
+  else
+    k.template run_single<SIGN, false, true>(tid);
 }
 
 #endif

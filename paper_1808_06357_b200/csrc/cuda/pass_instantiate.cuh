@@ -151,6 +151,17 @@ template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
     k.NT4 = G4::NT;
     k.smem4 = G4::smem;
   }
+  // the three-level inner passes (single transform, four-step twiddles on one
+  // side): forward + output twiddles, or input twiddles + inverse
+  if constexpr (LATTDSE_BUILD_PASS4 && AXIS == lattdse_dev::AX_COL && Geometry4<AXIS, L>::ok &&
+                ((PROG == lattdse_dev::PROG_LOADDIAG && SIGN == -1) || (PROG == lattdse_dev::PROG_STOREDIAG && SIGN == +1))) {
+    using G4 = Geometry4<AXIS, L>;
+    k.fn4[0] = reinterpret_cast<const void*>(
+        &lattdse_dev::fft_single4_kernel<L, G4::B, G4::PP, G4::NT, SIGN, PROG == lattdse_dev::PROG_STOREDIAG, G4::MB>);
+    k.B4 = G4::B;
+    k.NT4 = G4::NT;
+    k.smem4 = G4::smem;
+  }
   register_pass_kernel(AXIS, L, PROG, SIGN, k);
 }
 

@@ -574,6 +574,8 @@ struct Solver::Impl {
       const int v4 = pass4_variant(axis, L, k, a, nlines);
       if (v4 >= 0) return launch_pass4(axis, L, k, v4, a, nlines, nbatch);
     }
+    if (use_pass4 && prog != PROG_DOUBLE && nbatch <= 65535 && pass4_single_ok(axis, L, prog, k, a, nlines))
+      return launch_pass4(axis, L, k, 0, a, nlines, nbatch);
     const void* fn = k->fn;
     if (prog == PROG_DOUBLE) {
       const int mb = k->default_mb;
@@ -662,6 +664,18 @@ struct Solver::Impl {
     if (a.diag_kind == DG_CPLX && a.pre_tw && a.post_tw) return 0;
     if (a.diag_kind == DG_LUT16 && !a.pre_tw && !a.post_tw && k->fn4[1]) return 1;
     return -1;
+  }
+  // the lean single-transform kernel (fft_single4_kernel): plain COL layout,
+  // no diagonal, four-step twiddles on the output (forward) or input
+  // (inverse) side only -- the inner passes of the three-level layout
+  bool pass4_single_ok(int axis, int L, int prog, const dev::PassKernel* k, const PassArgs& a, long long nlines) const {
+    if (axis != AX_COL || !k->fn4[0] || a.diag_kind != DG_NONE || a.pfa || a.rb_w > 0 || a.ncols_g > 0 ||
+        a.col_off != 0 || a.obs)
+      return false;
+    if (nlines % k->B4 != 0 || nlines != a.ncols) return false;
+    const long long span = (long long)L * a.ncols;
+    if (a.nvalid_in < span || a.nvalid_out < span || a.in_bstride < span || a.out_bstride < span) return false;
+    return prog == PROG_LOADDIAG ? (a.post_tw && !a.pre_tw) : (a.pre_tw && !a.post_tw);
   }
   void launch_pass4(int axis, int L, dev::PassKernel* k, int v4, PassArgs a, long long nlines, long long nbatch) {
     if (!k->attr4_set) {
