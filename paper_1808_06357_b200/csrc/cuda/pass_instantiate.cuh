@@ -54,11 +54,16 @@ template <int AXIS, int L> struct Geometry {
 // columns 262 vs v1 303 on config 2, ROW 2048 139 vs v1 219); the few such
 // plans the swizzle cannot keep affine (512, 1024: a radix-2 / 4 end stage
 // behind radix 16) stay on the v1 kernels.
-template <int AXIS, int L> struct Geometry4 {
+// WIDE: the eight-column variant of short COL lines (L <= 648), used when the
+// rows of the view lie megabytes apart (config 4's first-level pass: row
+// stride 70 MB, every 64-byte segment its own DRAM page; 128-byte segments
+// 32.1 vs 35.2 ms per launch), while config 3 (row stride 17 KB) keeps four
+// columns (equal in the sustained bench, 5% faster at boost clocks)
+template <int AXIS, int L, bool WIDE = false> struct Geometry4 {
   using P = lattdse_dev::Plan<L>;
   static constexpr bool row = AXIS == lattdse_dev::AX_ROW;
-  static constexpr bool ok = P::nst >= 2 && L >= 64 && lattdse_dev::P4Seq<L>::swz_ok();
-  static constexpr int B = row ? (L >= 512 ? 1 : (L >= 256 ? 2 : 256 / L * 2)) : (L <= 648 ? 4 : 2);
+  static constexpr bool ok = P::nst >= 2 && L >= 64 && lattdse_dev::P4Seq<L>::swz_ok() && (!WIDE || (!row && L <= 648));
+  static constexpr int B = row ? (L >= 512 ? 1 : (L >= 256 ? 2 : 256 / L * 2)) : (L <= 648 ? (WIDE ? 8 : 4) : 2);
   // threads: the multiple of 32 with the fewest thread slots over the stage
   // sequence (a stage of t tasks runs ceil(t / NT) rounds of NT threads,
   // each task R elements of work; the fused mid stage runs once with two
@@ -150,6 +155,13 @@ template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
     k.B4 = G4::B;
     k.NT4 = G4::NT;
     k.smem4 = G4::smem;
+    if constexpr (Geometry4<AXIS, L, true>::ok) {
+      using GW = Geometry4<AXIS, L, true>;
+      k.fn4w = reinterpret_cast<const void*>(&fft_pass4_kernel<AXIS, L, GW::B, 1, GW::PP, GW::NT, SIGN, true, DG_CPLX, GW::MB>);
+      k.B4w = GW::B;
+      k.NT4w = GW::NT;
+      k.smem4w = GW::smem;
+    }
   }
   // the three-level inner passes (single transform, four-step twiddles on one
   // side): forward + output twiddles, or input twiddles + inverse

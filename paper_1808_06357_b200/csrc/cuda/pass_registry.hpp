@@ -22,6 +22,10 @@ struct PassKernel {
   const void* fn4[2] = {};
   int B4 = 0, NT4 = 0, smem4 = 0;
   bool attr4_set = false;
+  // short COL lines: the eight-column variant of fn4[0] for views whose rows
+  // lie far apart (pass_instantiate.cuh Geometry4 WIDE)
+  const void* fn4w = nullptr;
+  int B4w = 0, NT4w = 0, smem4w = 0;
   // PROG_DOUBLE instantiated with __launch_bounds__(NT, minBlocks) for
   // minBlocks = 1..4 (register cap vs occupancy); index 0 unused
   const void* fn_mb[5] = {};

@@ -572,10 +572,10 @@ struct Solver::Impl {
     a.nlines = (int)nlines;
     if (use_pass4 && prog == PROG_DOUBLE && nbatch <= 65535) {
       const int v4 = pass4_variant(axis, L, k, a, nlines);
-      if (v4 >= 0) return launch_pass4(axis, L, k, v4, a, nlines, nbatch);
+      if (v4 >= 0) return launch_pass4(axis, L, prog, k, v4, a, nlines, nbatch);
     }
     if (use_pass4 && prog != PROG_DOUBLE && nbatch <= 65535 && pass4_single_ok(axis, L, prog, k, a, nlines))
-      return launch_pass4(axis, L, k, 0, a, nlines, nbatch);
+      return launch_pass4(axis, L, prog, k, 0, a, nlines, nbatch);
     const void* fn = k->fn;
     if (prog == PROG_DOUBLE) {
       const int mb = k->default_mb;
@@ -677,10 +677,11 @@ struct Solver::Impl {
     if (a.nvalid_in < span || a.nvalid_out < span || a.in_bstride < span || a.out_bstride < span) return false;
     return prog == PROG_LOADDIAG ? (a.post_tw && !a.pre_tw) : (a.pre_tw && !a.post_tw);
   }
-  void launch_pass4(int axis, int L, dev::PassKernel* k, int v4, PassArgs a, long long nlines, long long nbatch) {
+  void launch_pass4(int axis, int L, int prog, dev::PassKernel* k, int v4, PassArgs a, long long nlines, long long nbatch) {
     if (!k->attr4_set) {
       for (const void* f : k->fn4)
         if (f) LD_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem4));
+      if (k->fn4w) LD_CK(cudaFuncSetAttribute(k->fn4w, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem4w));
       k->attr4_set = true;
     }
     a.nlines = (int)nlines;
@@ -688,17 +689,26 @@ struct Solver::Impl {
     a.mid_rb = (int)std::min<long long>(nmid / a.ncols, 0x7fffffff);
     a.mid_cb = (int)(nmid % a.ncols);
     a.pf = pass4_pf;
-    const dim3 grid((unsigned)(nlines / k->B4), (unsigned)nbatch);
-    void* args[] = {&a};
+    int B4 = k->B4, NT4 = k->NT4, smem4 = k->smem4;
     const void* fn = k->fn4[v4];
+    // rows of the view a megabyte or more apart: eight columns per CTA
+    if (prog == PROG_DOUBLE && v4 == 0 && axis == AX_COL && k->fn4w && (long long)a.ncols * 16 >= (1LL << 20) &&
+        nlines % k->B4w == 0) {
+      fn = k->fn4w;
+      B4 = k->B4w;
+      NT4 = k->NT4w;
+      smem4 = k->smem4w;
+    }
+    const dim3 grid((unsigned)(nlines / B4), (unsigned)nbatch);
+    void* args[] = {&a};
     const bool persist_this = persist_bytes > 0 && a.diag_kind == DG_CPLX &&
                               ((axis == AX_ROW && (persist_mode & 1)) || (axis == AX_COL && (persist_mode & 2)));
     if (persist_this) {
       // keep the per-step diagonal table L2-resident (see launch_pass)
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = grid;
-      cfg.blockDim = dim3(k->NT4);
-      cfg.dynamicSmemBytes = (size_t)k->smem4;
+      cfg.blockDim = dim3(NT4);
+      cfg.dynamicSmemBytes = (size_t)smem4;
       cfg.stream = stream;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
@@ -711,7 +721,7 @@ struct Solver::Impl {
       cfg.numAttrs = 1;
       LD_CK(cudaLaunchKernelExC(&cfg, fn, args));
     } else {
-      LD_CK(cudaLaunchKernel(fn, grid, dim3(k->NT4), args, (size_t)k->smem4, stream));
+      LD_CK(cudaLaunchKernel(fn, grid, dim3(NT4), args, (size_t)smem4, stream));
     }
     ++launches;
     ++launches4;
