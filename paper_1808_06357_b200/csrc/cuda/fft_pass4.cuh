@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(NT, MINB) fft_pass4_kernel(const __grid_consta
 // PRE: conjugate twiddles at the load (elements j + r T0 of the first
 // stage); POST: twiddles at the store (elements j + r T of the last stage).
 template <int L, int B, bool PP, int NT, int SIGN, bool PRE, int MINB>
-__global__ void __launch_bounds__(NT, MINB) fft_single4_kernel(const __grid_constant__ PassArgs a) {
+__global__ void __launch_bounds__(NT, MINB) fft_pass4s_kernel(const __grid_constant__ PassArgs a) {
   using K = Pass4<AX_COL, L, B, 1, PP, NT, SIGN, true, DG_NONE>;
   using G = typename K::G;
   extern __shared__ double2 lattdse_smem4[];

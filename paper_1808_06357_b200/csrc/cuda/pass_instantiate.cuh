@@ -169,7 +169,7 @@ template <int AXIS, int L, int PROG, int SIGN> void reg_one() {
                 ((PROG == lattdse_dev::PROG_LOADDIAG && SIGN == -1) || (PROG == lattdse_dev::PROG_STOREDIAG && SIGN == +1))) {
     using G4 = Geometry4<AXIS, L>;
     k.fn4[0] = reinterpret_cast<const void*>(
-        &lattdse_dev::fft_single4_kernel<L, G4::B, G4::PP, G4::NT, SIGN, PROG == lattdse_dev::PROG_STOREDIAG, G4::MB>);
+        &lattdse_dev::fft_pass4s_kernel<L, G4::B, G4::PP, G4::NT, SIGN, PROG == lattdse_dev::PROG_STOREDIAG, G4::MB>);
     k.B4 = G4::B;
     k.NT4 = G4::NT;
     k.smem4 = G4::smem;

@@ -665,7 +665,7 @@ struct Solver::Impl {
     if (a.diag_kind == DG_LUT16 && !a.pre_tw && !a.post_tw && k->fn4[1]) return 1;
     return -1;
   }
-  // the lean single-transform kernel (fft_single4_kernel): plain COL layout,
+  // the lean single-transform kernel (fft_pass4s_kernel): plain COL layout,
   // no diagonal, four-step twiddles on the output (forward) or input
   // (inverse) side only -- the inner passes of the three-level layout
   bool pass4_single_ok(int axis, int L, int prog, const dev::PassKernel* k, const PassArgs& a, long long nlines) const {

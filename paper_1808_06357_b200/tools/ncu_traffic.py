@@ -57,6 +57,9 @@ def main(tag, configs=("C2", "C3", "C4")):
         m1, lps = sol["M1"], sol["launches_per_step"]
         launches = []
         for name, v in load(csvp):
+            if "fft_pass4s_kernel" in name:  # lean single-transform pass (three-level inner passes): row side
+                launches.append((False, v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum", 0.0)))
+                continue
             t = re.search(r"fft_pass(4?)_kernel<([^>]*)>", name)
             if t:
                 # v1: <axis, L, B, NT, prog, sign, minb>; pass4 (always the double program):
