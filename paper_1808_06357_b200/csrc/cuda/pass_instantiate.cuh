@@ -37,8 +37,9 @@ template <int AXIS, int L> struct Geometry {
 // pass4 launch geometry per (axis, L), from the sweeps of fft_pass4_devtest
 // (profiles/r2/p4_sweep*.txt; us per launch, config-3 shapes over 64 members
 // unless noted):
-//  ROW: one line per CTA (two below 512, more for short lines), two stage
-//       buffers (one barrier per stage) while both fit 72 KB;
+//  ROW: one line per CTA (two below 512, more for short lines); two stage
+//       buffers (one barrier per stage) for plans with a radix above 12
+//       while both fit 72 KB, in place otherwise;
 //  COL: more, smaller CTAs beat wider tiles -- L <= 648: four adjacent
 //       columns (64-byte row segments) in place, COL 486 four CTAs of 224
 //       threads 348 vs two CTAs of eight columns 366 vs v1 441; longer
@@ -101,7 +102,7 @@ template <int AXIS, int L, bool WIDE = false> struct Geometry4 {
     for (int s = 0; s < P::nst; ++s) m = P::radix(s) > m ? P::radix(s) : m;
     return m;
   }
-  static constexpr int ip_budget = big ? 128 : (max_radix() >= 15 ? 96 : 72);
+  static constexpr int ip_budget = big ? 128 : (max_radix() >= 15 ? 96 : (row ? 80 : 72));
   static constexpr int fit(int bytes) { return (227 * 1024) / (bytes + 1024) > 0 ? (227 * 1024) / (bytes + 1024) : 1; }
   static constexpr int regs_ctas(int budget) { return 65536 / (NT * budget) > 0 ? 65536 / (NT * budget) : 1; }
   static constexpr int bytes_pp = lattdse_dev::P4Geom<AXIS, L, B, 1, true>::bytes;
@@ -111,7 +112,9 @@ template <int AXIS, int L, bool WIDE = false> struct Geometry4 {
   // CTAs as the registers allow (ROW 2048: in place at 4 CTAs 139 us, two
   // buffers at 3 CTAs 180 us over 4 x 2048 lines); COL above 648 while both
   // fit 90 KB (config 1, COL 1296: 35.0 vs 39.0 us), short COL lines in place
-  static constexpr bool PP = row ? (bytes_pp <= 72 * 1024 && fit(bytes_pp) >= regs_ctas(big ? 128 : 96))
+  // (ROW lines of small radices run in place as well: 1080 at 6 CTAs of 80
+  // registers 262.7 us, two buffers at 5 CTAs of 94 registers 270.6 us)
+  static constexpr bool PP = row ? (max_radix() > 12 && bytes_pp <= 72 * 1024 && fit(bytes_pp) >= regs_ctas(big ? 128 : 96))
                                  : (L > 648 && bytes_pp <= 90 * 1024);
   static constexpr int smem = PP ? bytes_pp : bytes_ip;
   static constexpr int by_regs = regs_ctas(PP ? (big ? 128 : 96) : ip_budget);
