@@ -166,7 +166,7 @@ template <int AXIS, int L, int B, int LPT, bool PP, int NT, int SIGN1, bool TW, 
   }
   // four-step twiddles of task j, line b (elements j + r T0): base * twp[b][r]
   template <int R, bool CONJ> __device__ __forceinline__ void fourstep(int b, int j, double2 (&v)[R]) const {
-    const double2 base = twid((long long)(line0 + b) * twm * j);
+    const double2 base = twid((long long)(a.col_off + line0 + b) * twm * j);
     const double2* p = twp + b * R;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(NT, MINB) fft_pass4_kernel(const __grid_consta
     constexpr int R0 = G::R0, T0 = L / R0;
     for (int i = tid; i < B * R0; i += NT) {
       const int b = i / R0, r = i - b * R0;
-      twp[i] = k.twid((long long)(line0 + b) * (T0 * r));
+      twp[i] = k.twid((long long)(a.col_off + line0 + b) * (T0 * r));
     }
   }
   k.run(tid);
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(NT, MINB) fft_pass4s_kernel(const __grid_const
   static_assert(B * Rt <= G::tw_slots, "twiddle slots");
   for (int i = tid; i < B * Rt; i += NT) {
     const int b = i / Rt, r = i - b * Rt;
-    twp[i] = k.twid((long long)(line0 + b) * k.twm * (Tt * r));
+    twp[i] = k.twid((long long)(a.col_off + line0 + b) * k.twm * (Tt * r));
   }
   if (PRE)
     k.template run_single<SIGN, true, false>(tid);

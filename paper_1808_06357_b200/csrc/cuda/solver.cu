@@ -654,7 +654,7 @@ struct Solver::Impl {
   // instantiations cover (fft_pass4.cuh); everything else stays on v1.
   // Returns the fn4 index or -1.
   int pass4_variant(int axis, int L, const dev::PassKernel* k, const PassArgs& a, long long nlines) const {
-    if (!k->fn4[0] || a.pfa || a.rb_w > 0 || a.ncols_g > 0 || a.col_off != 0 || a.tw_mul > 1 || a.obs) return -1;
+    if (!k->fn4[0] || a.pfa || a.rb_w > 0 || a.ncols_g > 0 || a.tw_mul > 1 || a.obs) return -1;
     if (nlines % k->B4 != 0) return -1;
     const long long span = axis == AX_COL ? (long long)L * a.ncols : nlines * (long long)L;
     if (axis == AX_COL && nlines != a.ncols) return -1;

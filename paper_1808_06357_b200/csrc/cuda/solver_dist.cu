@@ -282,6 +282,7 @@ struct DistSolver::Impl {
   int tw_shift = 0;
   ncclComm_t comm = nullptr;
   bool have_dt = false;
+  long long launches4 = 0;  // passes that ran on the lean kernels
   // row side in `chunks` row chunks (Hb % chunks == 0): the exchanges run on
   // their own stream, chunk by chunk, under the row passes of the other
   // chunks; 1: one blocking exchange each way
@@ -298,6 +299,33 @@ struct DistSolver::Impl {
   void launch(int axis, int L, int prog, int sign, PassArgs a, long long nlines, long long nbatch = 1) {
     dev::PassKernel* k = dev::find_pass_kernel(axis, L, prog, sign);
     if (!k) raise(Errc::unsupported, "no pass kernel for L=" + std::to_string(L));
+    // the lean per-step kernel (fft_pass4.cuh) where the slab pass is a plain
+    // layout: the COL pass of a column slab (global column offset only enters
+    // the four-step twiddles) and the ROW pass over contiguous lines (three-
+    // level rows); block-major rows and the inner COL passes stay generic
+    static const bool use_pass4 = !(std::getenv("LATTDSE_PASS4") && std::atoi(std::getenv("LATTDSE_PASS4")) == 0);
+    if (use_pass4 && prog == PROG_DOUBLE && k->fn4[0] && a.diag_kind == DG_CPLX && a.rb_w == 0 && !a.pfa &&
+        a.ncols_g == 0 && a.tw_mul <= 1 && !a.obs && nlines % k->B4 == 0 && nbatch <= 65535 &&
+        (axis == AX_ROW ? (!a.pre_tw && !a.post_tw) : (a.pre_tw && a.post_tw && nlines == a.ncols))) {
+      const long long span = axis == AX_COL ? (long long)L * a.ncols : nlines * (long long)L;
+      if (a.nvalid_in >= span && a.nvalid_out >= span && a.nvalid_mid >= span) {
+        if (!k->attr4_set) {
+          for (const void* f : k->fn4)
+            if (f) LD_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem4));
+          if (k->fn4w) LD_CK(cudaFuncSetAttribute(k->fn4w, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem4w));
+          k->attr4_set = true;
+        }
+        a.nlines = (int)nlines;
+        a.mid_rb = L;  // no mid mask (it is folded into the slab tables)
+        a.mid_cb = 0;
+        a.pf = 0;
+        void* args4[] = {&a};
+        LD_CK(cudaLaunchKernel(k->fn4[0], dim3((unsigned)(nlines / k->B4), (unsigned)nbatch), dim3(k->NT4), args4,
+                               (size_t)k->smem4, stream));
+        ++launches4;
+        return;
+      }
+    }
     const void* fn = k->fn;
     if (prog == PROG_DOUBLE && k->fn_mb[k->default_mb]) fn = k->fn_mb[k->default_mb];
     if (!k->attr_set) {
