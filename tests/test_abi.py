@@ -114,3 +114,23 @@ def test_pass_kernel_emulation():
                    stdout=subprocess.DEVNULL)
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ALL OK" in out.stdout, out.stdout[-2000:]
+
+
+def test_lean_kernel_launch_geometry():
+    """Compile-time launch geometry of the lean per-step kernels for the lengths
+    the five configs run (pass_instantiate.cuh Geometry4): the measured choices
+    of profiles/r2/p4_sweep*.txt, and which plans take the swizzled slots."""
+    csrc = os.path.join(ROOT, "paper_1808_06357_b200", "csrc")
+    subprocess.run(["make", "-C", csrc, "geomtest"], check=True, stdout=subprocess.DEVNULL)
+    out = subprocess.run([os.path.join(csrc, "build", "pass4_geomtest")], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, out.stderr
+    rows = {int(line.split()[0][2:]): line for line in out.stdout.splitlines() if line.startswith("L=")}
+    # config 3: COL 486 four columns in place, 4 CTAs of 224 threads (+ the eight-column variant); ROW 1080 (9,12,10) in place, 6 CTAs of 128
+    assert "plan 9 9 6 ok=1 swz=0" in rows[486] and "COL B=4 pp=0 NT=224 MB=4" in rows[486] and "WIDE ok=1 B=8 NT=448 MB=2" in rows[486]
+    assert "plan 9 12 10 ok=1 swz=0" in rows[1080] and "ROW B=1 pp=0 NT=128 MB=6" in rows[1080]
+    # config 1: COL 1296 two columns with two stage buffers; ROW 1620 two buffers at 3 CTAs
+    assert "COL B=2 pp=1 NT=288 MB=2" in rows[1296] and "ROW B=1 pp=1 NT=192 MB=3" in rows[1620]
+    # power-of-two plans run swizzled (config 2's 4096, config 4's 2048-long rows); 512 / 1024 stay on the generic kernels
+    assert "ok=1 swz=1" in rows[4096] and "ROW B=1 pp=0 NT=256 MB=2" in rows[4096] and "COL B=2 pp=0 NT=512 MB=1" in rows[4096]
+    assert "ok=1 swz=1" in rows[2048] and "ROW B=1 pp=0 NT=128 MB=4" in rows[2048]
+    assert "ok=0" in rows[512] and "ok=0" in rows[1024]
